@@ -1,0 +1,77 @@
+"""The five BASELINE.json presets (BASELINE.json "configs").
+
+Notation follows BASELINE.json: M = BS antennas (paper's R),
+K = users (paper's S), N = used subcarriers, L = PDP tap count (paper's M).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+
+@dataclass(frozen=True)
+class Config:
+    cfg_id: int
+    name: str
+    M: int                 # BS antennas
+    K: int                 # users (time-orthogonal pilots, one symbol per user)
+    N: int                 # used subcarriers, contiguous tones 0..N-1 (reading A10)
+    Nfft: int
+    slots: int
+    pilots_per_slot: int   # estimation instances per slot (reading A3)
+    b: int                 # block / window length
+    stride: int            # window stride s (== b: non-overlapping)
+    n_taps: int            # L, exponential PDP tap count (3 dB/tap, reading A6)
+    tap_spacing: Optional[float] = None            # fixed delay spacing in samples (configs 1-2)
+    tau_rms_s: Optional[float] = None              # fixed rms delay spread (configs 3, 5)
+    tau_rms_range_s: Optional[Tuple[float, float]] = None  # per-slot U[lo, hi] (config 4)
+    fs_hz: Optional[float] = None                  # sampling rate Nfft * subcarrier spacing
+    snr_db: Optional[float] = None                 # fixed SNR
+    snr_choice_db: Optional[Tuple[float, ...]] = None      # per-slot choice (config 2)
+    snr_range_db: Optional[Tuple[float, float]] = None     # per-slot U[lo, hi] (config 4)
+    per_slot_stats: bool = False                   # reading A4: matched per-slot statistics
+
+    @property
+    def T(self) -> int:
+        """Estimation instances = slots x pilot symbols per slot."""
+        return self.slots * self.pilots_per_slot
+
+    @property
+    def n_sets(self) -> int:
+        return self.slots if self.per_slot_stats else 1
+
+    @property
+    def cols(self) -> int:
+        return self.M * self.K
+
+    @property
+    def estimates(self) -> int:
+        """E = M*K*N*T channel estimates (antenna x user x subcarrier x instance)."""
+        return self.M * self.K * self.N * self.T
+
+
+CONFIGS = {
+    1: Config(1, "tiny", M=8, K=2, N=72, Nfft=128, slots=1, pilots_per_slot=1,
+              b=12, stride=12, n_taps=4, tap_spacing=1.0, snr_db=10.0),
+    2: Config(2, "small", M=32, K=4, N=300, Nfft=512, slots=2, pilots_per_slot=1,
+              b=50, stride=25, n_taps=8, tap_spacing=1.0,
+              snr_choice_db=(0.0, 10.0, 20.0), per_slot_stats=True),
+    3: Config(3, "paper", M=128, K=12, N=1200, Nfft=2048, slots=1, pilots_per_slot=1,
+              b=100, stride=100, n_taps=16, tau_rms_s=1e-6, fs_hz=30.72e6, snr_db=15.0),
+    4: Config(4, "paper_batched", M=128, K=12, N=1200, Nfft=2048, slots=20, pilots_per_slot=2,
+              b=150, stride=100, n_taps=16, tau_rms_range_s=(0.3e-6, 2e-6), fs_hz=30.72e6,
+              snr_range_db=(0.0, 25.0), per_slot_stats=True),
+    5: Config(5, "scale_out", M=256, K=24, N=3276, Nfft=4096, slots=20, pilots_per_slot=1,
+              b=126, stride=126, n_taps=24, tau_rms_s=0.5e-6, fs_hz=122.88e6, snr_db=20.0),
+}
+
+
+def get_config(cfg) -> Config:
+    if isinstance(cfg, Config):
+        return cfg
+    if isinstance(cfg, str):
+        for c in CONFIGS.values():
+            if c.name == cfg:
+                return c
+        return CONFIGS[int(cfg)]
+    return CONFIGS[int(cfg)]
