@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the block-LMMSE pilot channel estimator (arXiv 1802.05427 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One step = one pass of the hot path (LS + block-LMMSE contraction, a3-a5 of SURVEY.md §8(a))
+over one estimation batch of the configured workload (default: config 3, the paper-scale
+128 x 12 x 1200 slot, b = 100).  The filters W_b (a1-a2) are per-statistics, precomputed
+before the slot loop exactly as the paper does offline; their
+build time is reported separately as `filter_build_ms`.
+
+Multi-GPU (torchrun, one rank per GPU): each rank estimates its own batch (antenna-sharded
+global batch, no data-path collective) -> weak scaling; time = max over ranks.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §6 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402  (seeded input generator: no estimator arithmetic)
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _cfg_json(cfg, extra):
+    d = {"workload": f"config{cfg.cfg_id}_{cfg.name}_{cfg.M}x{cfg.K}x{cfg.N}_T{cfg.T}_b{cfg.b}_s{cfg.stride}",
+         "M": cfg.M, "K": cfg.K, "N": cfg.N, "T": cfg.T, "b": cfg.b, "stride": cfg.stride,
+         "n_sets": cfg.n_sets}
+    d.update(extra)
+    return d
+
+
+def _oracle_rate(cfg, x, y, r, s2, soi, budget_s: float, min_runs: int = 3):
+    """Time the oracle's LS + block apply (no generation, no filter build) on (y, x)."""
+    import oracle
+    filters = {}
+    for st in set(int(v) for v in soi):
+        filters[st] = [oracle.block_filter(r[st], s2[st], cfg.b)] * len(oracle.window_table(cfg.N, cfg.b, cfg.stride))
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        H_ls = oracle.ls_estimate(y, x)
+        for t in range(y.shape[0]):
+            oracle.block_apply(H_ls[t], filters[int(soi[t])], cfg.b, cfg.stride)
+        runs += 1
+        el = time.perf_counter() - t0
+        if runs >= min_runs and el >= budget_s:
+            break
+    return runs, el
+
+
+def _cores():
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        if os.environ.get(var):
+            return int(os.environ[var])
+    return len(os.sched_getaffinity(0))
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle (the slow program the ratio divides by), rank 0 only."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    x = workload.gen_pilots(cfg, 0)
+    r, s2 = workload.channel_stats(cfg, 0)
+    soi = workload.set_of_instance(cfg)
+    # bounded sample: antennas [0, m) of instance 0, sized for <= ~0.03 s of oracle work per step
+    m = max(1, min(cfg.M, args.ref_antennas))
+    y = workload.gen_instances(cfg, 0, t_lo=0, t_hi=1, m_lo=0, m_hi=m, x=x[:1])
+    import oracle
+    filters = [oracle.block_filter(r[soi[0]], s2[soi[0]], cfg.b)] * len(oracle.window_table(cfg.N, cfg.b, cfg.stride))
+
+    def step():
+        H_ls = oracle.ls_estimate(y, x[:1])
+        oracle.block_apply(H_ls[0], filters, cfg.b, cfg.stride)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    est = m * cfg.K * cfg.N
+    value = est * args.steps / el
+    sample = f"oracle LS+block apply (complex128 NumPy/OpenBLAS) on antennas [0,{m}) of config {cfg.cfg_id} instance 0 per step"
+    line = {
+        "impl": "reference", "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value,
+        "unit": "estimates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workload generator)",
+        "config": _cfg_json(cfg, {"sample_antennas": m}),
+        "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": _cores(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_05427_b200 as ce
+
+    world, rank, local = _dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    r, s2 = workload.channel_stats(cfg, 0)
+    soi = workload.set_of_instance(cfg)
+    x = workload.gen_pilots(cfg, 0)
+    # rank r estimates antennas of its own shard of the global batch: seeded by rank
+    y = workload.gen_instances(cfg, 0 + rank, x=x)
+    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2, kernel=args.kernel)
+    stream = torch.cuda.current_stream()
+    tb0 = time.perf_counter()
+    est.build()
+    build_ms = (time.perf_counter() - tb0) * 1e3
+
+    # inputs larger than L2: rotate over nbuf (y, h) buffer pairs, total > 126 MB
+    step_bytes = 2 * y.nbytes
+    nbuf = max(2, int(np.ceil(1.25 * L2_BYTES / step_bytes)) + 1)
+    y_dev = [torch.from_numpy(y).to(dev) for _ in range(nbuf)]
+    h_dev = [torch.empty_like(y_dev[0]) for _ in range(nbuf)]
+    x_dev = torch.from_numpy(x).to(dev)
+    soi_dev = torch.from_numpy(soi).to(dev)
+    T, M, K, N = y.shape
+    sptr = stream.cuda_stream
+
+    def step(i):
+        ce.ce_estimate(est.handle, y_dev[i % nbuf].data_ptr(), x_dev.data_ptr(), h_dev[i % nbuf].data_ptr(),
+                       T, M, K, soi_dev.data_ptr(), sptr)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = est.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = est.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    E = cfg.estimates
+    value = world * E * args.steps / (ms_max * 1e-3)
+    kernel_s = ms / args.steps * 1e-3      # one contraction launch per step on this stream
+
+    # end-to-end through the public host-buffer API: pinned host in, pinned host out
+    y_pin = torch.from_numpy(y).pin_memory()
+    x_pin = torch.from_numpy(x).pin_memory()
+    h_pin = torch.empty(y.shape, dtype=torch.complex64).pin_memory()
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        est.estimate_host(y_pin, x_pin, out=h_pin, set_of_instance=soi)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        est.estimate_host(y_pin, x_pin, out=h_pin, set_of_instance=soi)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * E * e2e_steps / (float(e2e_ms.item()) * 1e-3)
+
+    # roofline of the dominant kernel (the contraction): 8b flops per estimate, FP32 SIMT peak
+    props = torch.cuda.get_device_properties(dev)
+    peaks = _peaks()
+    sm_max = peaks.get("sm_max_mhz") or clk.summary().get("sm_max_mhz") or 1965.0
+    fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6     # FFMA lanes x 2 flops x clock
+    flops = 8.0 * cfg.b * E
+    achieved = flops / kernel_s
+    traffic = _ncu_traffic("k2_simt")
+    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak, "traffic": traffic,
+            "kernel": "k2_simt", "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz",
+            "algorithmic_bytes_per_launch": 16 * E + 8 * cfg.T * cfg.K * cfg.N,
+            "hbm_frac": (16 * E / kernel_s) / (peaks.get("hbm_gbs", 6548.8) * 1e9)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle  # noqa: F401  (cpu_baseline leg only)
+        m = max(1, min(cfg.M, args.ref_antennas * 4))
+        ys = y[:1, :m]
+        runs, el = _oracle_rate(cfg, x[:1], ys, r, s2, soi[:1], budget_s=args.cpu_budget_s)
+        cpu = {"value": runs * m * cfg.K * cfg.N / el, "unit": "estimates/s", "cores": _cores(), "kind": "oracle",
+               "sample": f"{runs} runs of oracle LS+block apply (complex128) on antennas [0,{m}) of config "
+                         f"{cfg.cfg_id} instance 0, {el:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value, "unit": "estimates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded workload generator, SURVEY.md §8(d) recipe)",
+            "config": _cfg_json(cfg, {"l2": f"rotating {nbuf} y/h buffer pairs ({nbuf * step_bytes / 2**20:.0f} MiB > L2)",
+                                      "kernel": {0: "auto", 1: "simt", 2: "tf32x3"}[args.kernel],
+                                      "global_batch_instances": world * cfg.T,
+                                      "parallelism": f"antenna/batch shard x{world}"}),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "estimates/s",
+                    "h2d_bytes_per_step": int(y.nbytes + x.nbytes + soi.nbytes),
+                    "d2h_bytes_per_step": int(y.nbytes), "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "filter_build_ms": build_ms,
+            "device": props.name,
+        }
+        print(json.dumps(line), flush=True)
+    est.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 simt, 2 tf32x3")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--ref-antennas", type=int, default=4)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = workload.get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * ce.h -- C ABI of libce, the B200 (sm_100a) block-LMMSE pilot channel estimator.
+ *
+ * Method (arXiv 1802.05427, "Implementation of Massive MIMO Uplink Receiver on
+ * RaPro Prototyping Platform"; line numbers refer to /root/reference/PAPER.md):
+ *
+ *   LS at the pilots        H_LS = Y / X                      PAPER.md:173-180 (Eq. 8-9), 438
+ *   block LMMSE filter      W_b  = R_b (R_b + sigma^2 I)^-1    PAPER.md:306-309 (Eq. 17), 345-349
+ *   block application       H    = W_b H_LS  per window        PAPER.md:186-190 (Eq. 12), 400-403
+ *
+ * generalised from the paper's 12x12 "12W" groups to
+ * b x b blocks of the N x N Toeplitz frequency autocorrelation R_hh, laid out as
+ * non-overlapping blocks (stride == b) or overlapping windows that keep their
+ * centre `stride` outputs (stride < b), with the paper's edge clamping
+ * (Table II).
+ *
+ * Window geometry (reading A7): n_windows = ceil((N-b)/stride) + 1;
+ * window w reads LS tones [a_w, a_w+b) with a_w = min(w*stride, N-b) and keeps
+ * outputs [o_w, o_{w+1}) with o_0 = 0, o_w = w*stride + floor((b-stride)/2),
+ * o_{n_windows} = N.  The kept ranges partition [0, N).
+ *
+ * Data layout (all complex values are interleaved {re, im}):
+ *   y  : complex64 [T][M][K][N]  received pilot symbols, antenna-major   (caller-owned)
+ *   x  : complex64 [T][K][N]     pilots, shared by all antennas           (caller-owned)
+ *   h  : complex64 [T][M][K][N]  channel estimates                        (caller-owned)
+ *   W  : complex64 [n_sets][b][b] filters, row-major                     (library-owned)
+ * T = estimation instances (slots x pilot symbols), M = BS antennas, K = users,
+ * N = subcarriers (contiguous tones 0..N-1, reading A10).
+ *
+ * Conventions
+ *   - Every function returns a ce_status (0 = OK, < 0 = error); ce_last_error()
+ *     gives a human-readable detail of the calling thread's last failure.
+ *   - A handle is bound to the CUDA device that is current at ce_init and is used
+ *     from one host thread at a time.  Multi-GPU = one handle per device/rank.
+ *   - `stream` arguments are cudaStream_t values passed as void* (NULL = legacy
+ *     default stream).  Device entry points are asynchronous on that stream.
+ *   - There is no CPU fallback: without a usable sm_100 device, calls that need the
+ *     GPU return CE_ENODEV / CE_ECUDA.
+ */
+#ifndef CE_H
+#define CE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CE_OK = 0,
+  CE_EINVAL = -1,  /* invalid argument: sizes, pointers, alignment, aliasing, sigma^2 */
+  CE_ENOMEM = -2,  /* host or device allocation failed */
+  CE_ECUDA = -3,   /* a CUDA runtime call failed (detail in ce_last_error) */
+  CE_ENOTPD = -4,  /* filter build: R_b + sigma^2 I not positive definite (Cholesky pivot <= 0 or NaN) */
+  CE_ESTATE = -5,  /* ce_estimate before a successful ce_build_filters */
+  CE_ENODEV = -6   /* no CUDA device, or not compute capability 10.x */
+} ce_status;
+
+typedef enum {
+  CE_KERNEL_AUTO = 0,   /* library picks the fastest kernel meeting the 1e-4 parity bar */
+  CE_KERNEL_SIMT = 1,   /* K2: FP32 SIMT complex FMA contraction */
+  CE_KERNEL_TF32X3 = 2  /* K3: tcgen05 kind::tf32, error-compensated hi/lo split (3 MMAs) */
+} ce_kernel;
+
+typedef struct ce_handle ce_handle; /* opaque */
+
+typedef struct {
+  int32_t N;      /* subcarriers, >= 1 */
+  int32_t b;      /* block / window length, 1 <= b <= N (b == N gives the full LMMSE) */
+  int32_t stride; /* window stride s, 1 <= s <= b: s == b non-overlapping, s < b overlapping */
+  int32_t n_sets; /* statistic sets, >= 1 (1 = the paper's fixed design) */
+  /* host, [n_sets][N][2] float64: Toeplitz first column r[d] = E{H(n+d) H*(n)}, d = 0..N-1,
+   * complex128 interleaved.  Only d < b is used by the filters; r[0]
+   * must be real and finite.  Copied by ce_init. */
+  const double *r_hh;
+  /* host, [n_sets] float64: sigma^2 / sigma_s^2 (Eq. 13), finite and > 0. Copied. */
+  const double *sigma2;
+} ce_params;
+
+/* Validate `p`, compute the window table on the host, copy the statistics to the
+ * current device and allocate W[n_sets][b][b] plus its workspace.
+ * Returns CE_EINVAL (nothing allocated, *out untouched) for: p or out NULL, N < 1,
+ * b < 1 or b > N, stride < 1 or stride > b, n_sets < 1, r_hh or sigma2 NULL,
+ * non-finite r_hh, r[0] not real and > 0, sigma2 <= 0 or non-finite.
+ * CE_ENODEV if no compute-capability-10 device is current; CE_ENOMEM on allocation failure. */
+int ce_init(const ce_params *p, ce_handle **out);
+
+/* K1 (Eq. 17; Cholesky as in the paper's cposv): per set,
+ * A = R_b + sigma^2 I from the Toeplitz first column, FP64 complex Cholesky A = L L^H,
+ * W = A^-1 R_b by forward/back substitution with b right-hand sides, rounded to complex64.
+ * Enqueued on `stream`, then synchronises that stream once to read the positive-definite flag.
+ * Returns CE_ENOTPD (handle stays unbuilt) if any pivot is <= 0 or not finite. */
+int ce_build_filters(ce_handle *h, void *stream);
+
+/* K2/K3 hot path (a3-a5 of SURVEY.md §8(a)): for every instance t, window w and column (m,k)
+ *   h[t,m,k, o_w:o_{w+1}] = W_{set(t)}[o_w-a_w : o_{w+1}-a_w, :] . (y[t,m,k, a_w:a_w+b] / x[t,k, a_w:a_w+b])
+ * with the LS division fused into the operand load.  Device pointers, asynchronous on
+ * `stream`: no allocation and no host synchronisation.
+ *   d_y, d_x, d_h : device, complex64, 8-byte aligned, layouts above; d_h must not overlap
+ *                   d_y or d_x.  Sub-tensors (e.g. an antenna shard [T][M'][K][N] with the
+ *                   matching instance range) are passed as offset pointers.
+ *   T, M, K       : >= 1.
+ *   d_set_of_instance : device int32 [T] with values in [0, n_sets), or NULL (all set 0).
+ *                   An out-of-range value makes that instance's outputs NaN.
+ * Returns CE_ESTATE before a successful ce_build_filters, CE_EINVAL for bad sizes, NULL or
+ * misaligned pointers and aliasing, CE_ECUDA if the launch fails. */
+int ce_estimate(ce_handle *h, const void *d_y, const void *d_x, void *d_h,
+                int32_t T, int32_t M, int32_t K, const int32_t *d_set_of_instance, void *stream);
+
+/* Same computation on HOST buffers (end-to-end path): copies y and x to device staging buffers
+ * owned by the handle (grown on demand), runs the hot path in antenna chunks pipelined over
+ * internal streams so host<->device copies overlap compute, copies h back, and returns after
+ * the results are in `h_host` (synchronous).  Pinned host memory gives full copy bandwidth.
+ * set_of_instance is HOST int32 [T] or NULL. */
+int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void *h_host,
+                     int32_t T, int32_t M, int32_t K, const int32_t *set_of_instance, void *stream);
+
+/* Free W, workspace, staging buffers and the handle.  NULL is allowed (no-op). */
+int ce_free(ce_handle *h);
+
+/* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value. */
+int ce_set_kernel(ce_handle *h, int32_t kernel);
+
+/* Copy the built filters to host memory: complex64 [n_sets][b][b] row-major (W[i][j] multiplies
+ * H_LS[a_w + j] for output a_w + i).  Synchronous.  CE_ESTATE if not built. */
+int ce_get_filters(ce_handle *h, void *host_W);
+
+/* Host-only (no CUDA): write the window table for (N, b, stride) as int32 triples
+ * {a_w, o_w, o_{w+1}} into out[0 .. 3*n_windows).  Returns n_windows (>= 1), or CE_EINVAL for
+ * invalid sizes or if capacity (in triples) < n_windows (out may be NULL to query the count
+ * with capacity 0 -> returns n_windows). */
+int ce_window_table(int32_t N, int32_t b, int32_t stride, int32_t *out, int32_t capacity);
+
+/* Number of CUDA kernels this handle has launched (K1 + K2/K3), for launch accounting. */
+int ce_launch_count(const ce_handle *h, int64_t *out);
+
+/* Static description of a status code; never NULL. */
+const char *ce_status_string(int status);
+
+/* Detail of the calling thread's last failed call ("" if none); never NULL. */
+const char *ce_last_error(void);
+
+/* Library version string, e.g. "libce 0.1 sm_100a". */
+const char *ce_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CE_H */

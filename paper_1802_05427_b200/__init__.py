@@ -1,0 +1,34 @@
+"""B200-native block-LMMSE pilot channel estimator (arXiv 1802.05427).
+
+The product path: libce.so (include/ce.h; CUDA kernels for sm_100a) behind a thin
+ctypes binding with the same function names.  No CPU fallback, no oracle import.
+"""
+from .ce import (  # noqa: F401
+    CE_EINVAL,
+    CE_ENODEV,
+    CE_ENOMEM,
+    CE_ENOTPD,
+    CE_ESTATE,
+    CE_KERNEL_AUTO,
+    CE_KERNEL_SIMT,
+    CE_KERNEL_TF32X3,
+    CE_OK,
+    EXPORTED,
+    CEError,
+    ChannelEstimator,
+    ce_build_filters,
+    ce_estimate,
+    ce_estimate_host,
+    ce_free,
+    ce_get_filters,
+    ce_init,
+    ce_last_error,
+    ce_launch_count,
+    ce_set_kernel,
+    ce_status_string,
+    ce_version,
+    ce_window_table,
+    window_table,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,246 @@
+"""ctypes binding of libce (include/ce.h) -- argument marshalling only.
+
+Every step of the estimator runs inside libce's CUDA kernels; this module only
+converts Python/NumPy/torch arguments to pointers and sizes.  There is no CPU
+fallback: importing this module fails loudly if libce.so has not been built.
+Function names match the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libce.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"libce.so not found at {_LIB_PATH}: build it with "
+        "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a)")
+
+lib = ctypes.CDLL(_LIB_PATH)
+
+CE_OK, CE_EINVAL, CE_ENOMEM, CE_ECUDA, CE_ENOTPD, CE_ESTATE, CE_ENODEV = 0, -1, -2, -3, -4, -5, -6
+CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3 = 0, 1, 2
+
+# every function declared in include/ce.h (tests check the .so exports all of them)
+EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+            "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
+            "ce_version")
+
+
+class ce_params(ctypes.Structure):
+    _fields_ = [("N", c_int32), ("b", c_int32), ("stride", c_int32), ("n_sets", c_int32),
+                ("r_hh", POINTER(c_double)), ("sigma2", POINTER(c_double))]
+
+
+lib.ce_init.argtypes = [POINTER(ce_params), POINTER(c_void_p)]
+lib.ce_build_filters.argtypes = [c_void_p, c_void_p]
+lib.ce_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]
+lib.ce_estimate_host.argtypes = lib.ce_estimate.argtypes
+lib.ce_free.argtypes = [c_void_p]
+lib.ce_set_kernel.argtypes = [c_void_p, c_int32]
+lib.ce_get_filters.argtypes = [c_void_p, c_void_p]
+lib.ce_window_table.argtypes = [c_int32, c_int32, c_int32, POINTER(c_int32), c_int32]
+lib.ce_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
+lib.ce_status_string.argtypes = [c_int]
+lib.ce_status_string.restype = c_char_p
+lib.ce_last_error.argtypes = []
+lib.ce_last_error.restype = c_char_p
+lib.ce_version.argtypes = []
+lib.ce_version.restype = c_char_p
+for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+           "ce_get_filters", "ce_window_table", "ce_launch_count"):
+    getattr(lib, _n).restype = c_int
+
+
+class CEError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {ce_status_string(status)} -- {ce_last_error()}")
+
+
+def _check(status: int, where: str) -> int:
+    if status < 0:
+        raise CEError(status, where)
+    return status
+
+
+def ce_status_string(status: int) -> str:
+    return lib.ce_status_string(status).decode()
+
+
+def ce_last_error() -> str:
+    return lib.ce_last_error().decode()
+
+
+def ce_version() -> str:
+    return lib.ce_version().decode()
+
+
+def ce_window_table(N: int, b: int, stride: int):
+    """Host-only window table [(a_w, o_w, o_{w+1}), ...] computed by the C++ library."""
+    n = _check(lib.ce_window_table(N, b, stride, None, 0), "ce_window_table")
+    buf = (c_int32 * (3 * n))()
+    _check(lib.ce_window_table(N, b, stride, buf, n), "ce_window_table")
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n)]
+
+
+window_table = ce_window_table
+
+
+def ce_init(N: int, b: int, stride: int, r_hh, sigma2) -> int:
+    """r_hh: complex [n_sets][N] (Toeplitz first columns); sigma2: float [n_sets]. Returns a handle."""
+    r = np.ascontiguousarray(np.asarray(r_hh, np.complex128).reshape(-1, N))
+    s2 = np.ascontiguousarray(np.asarray(sigma2, np.float64).reshape(-1))
+    n_sets = r.shape[0]
+    rv = r.view(np.float64)
+    p = ce_params(N, b, stride, n_sets if s2.shape[0] == n_sets else -1,
+                  rv.ctypes.data_as(POINTER(c_double)), s2.ctypes.data_as(POINTER(c_double)))
+    h = c_void_p()
+    _check(lib.ce_init(ctypes.byref(p), ctypes.byref(h)), "ce_init")
+    return h.value
+
+
+def ce_init_raw(N: int, b: int, stride: int, n_sets: int, r_ptr, s2_ptr) -> int:
+    """Unchecked-argument variant used by the ABI validation tests; returns the status."""
+    p = ce_params(N, b, stride, n_sets, ctypes.cast(r_ptr, POINTER(c_double)), ctypes.cast(s2_ptr, POINTER(c_double)))
+    h = c_void_p()
+    st = lib.ce_init(ctypes.byref(p), ctypes.byref(h))
+    if st == CE_OK:
+        lib.ce_free(h)
+    return st
+
+
+def ce_build_filters(h: int, stream: int = 0) -> None:
+    _check(lib.ce_build_filters(h, c_void_p(stream)), "ce_build_filters")
+
+
+def ce_estimate(h: int, d_y: int, d_x: int, d_h: int, T: int, M: int, K: int, d_soi: int = 0,
+                stream: int = 0) -> None:
+    _check(lib.ce_estimate(h, c_void_p(d_y), c_void_p(d_x), c_void_p(d_h), T, M, K,
+                           c_void_p(d_soi or None), c_void_p(stream)), "ce_estimate")
+
+
+def ce_estimate_host(h: int, y_ptr: int, x_ptr: int, h_ptr: int, T: int, M: int, K: int, soi_ptr: int = 0,
+                     stream: int = 0) -> None:
+    _check(lib.ce_estimate_host(h, c_void_p(y_ptr), c_void_p(x_ptr), c_void_p(h_ptr), T, M, K,
+                                c_void_p(soi_ptr or None), c_void_p(stream)), "ce_estimate_host")
+
+
+def ce_free(h: int) -> None:
+    _check(lib.ce_free(h), "ce_free")
+
+
+def ce_set_kernel(h: int, kernel: int) -> None:
+    _check(lib.ce_set_kernel(h, kernel), "ce_set_kernel")
+
+
+def ce_get_filters(h: int, n_sets: int, b: int) -> np.ndarray:
+    out = np.empty((n_sets, b, b), np.complex64)
+    _check(lib.ce_get_filters(h, out.ctypes.data), "ce_get_filters")
+    return out
+
+
+def ce_launch_count(h: int) -> int:
+    v = c_int64()
+    _check(lib.ce_launch_count(h, ctypes.byref(v)), "ce_launch_count")
+    return v.value
+
+
+class ChannelEstimator:
+    """Owns one libce handle (one device).  torch tensors in, torch tensors out.
+
+    est = ChannelEstimator(N, b, stride, r_hh, sigma2); est.build()
+    h = est.estimate(y, x)            # y complex64 cuda [T][M][K][N], x [T][K][N]
+    """
+
+    def __init__(self, N: int, b: int, stride: int, r_hh, sigma2, kernel: int = CE_KERNEL_AUTO):
+        self.N, self.b, self.stride = int(N), int(b), int(stride)
+        self.n_sets = int(np.asarray(sigma2).reshape(-1).shape[0])
+        self.handle = ce_init(N, b, stride, r_hh, sigma2)
+        if kernel != CE_KERNEL_AUTO:
+            ce_set_kernel(self.handle, kernel)
+
+    def build(self, stream=None) -> "ChannelEstimator":
+        ce_build_filters(self.handle, _stream_ptr(stream))
+        return self
+
+    def filters(self) -> np.ndarray:
+        return ce_get_filters(self.handle, self.n_sets, self.b)
+
+    def estimate(self, y, x, out=None, set_of_instance=None, stream=None):
+        import torch
+        if y.dtype != torch.complex64 or x.dtype != torch.complex64:
+            raise TypeError("y and x must be complex64")
+        if not (y.is_cuda and x.is_cuda):
+            raise TypeError("ChannelEstimator.estimate takes CUDA tensors; use estimate_host for host arrays")
+        T, M, K, N = y.shape
+        if N != self.N or tuple(x.shape) != (T, K, N):
+            raise ValueError(f"shape mismatch: y {tuple(y.shape)}, x {tuple(x.shape)}, N={self.N}")
+        if not (y.is_contiguous() and x.is_contiguous()):
+            raise ValueError("y and x must be contiguous")
+        if out is None:
+            out = torch.empty_like(y)
+        soi = 0
+        if set_of_instance is not None:
+            if set_of_instance.dtype != torch.int32 or not set_of_instance.is_cuda:
+                raise TypeError("set_of_instance must be a CUDA int32 tensor")
+            soi = set_of_instance.data_ptr()
+        ce_estimate(self.handle, y.data_ptr(), x.data_ptr(), out.data_ptr(), T, M, K, soi, _stream_ptr(stream))
+        return out
+
+    def estimate_host(self, y: np.ndarray, x: np.ndarray, out: np.ndarray = None, set_of_instance=None,
+                      stream=None):
+        """End-to-end path through ce_estimate_host: host (NumPy or pinned torch) buffers in and out."""
+        T, M, K, N = y.shape
+        if out is None:
+            out = np.empty(y.shape, np.complex64)
+        soi_ptr = 0
+        if set_of_instance is not None:
+            set_of_instance = np.ascontiguousarray(set_of_instance, np.int32)
+            soi_ptr = set_of_instance.ctypes.data
+        ce_estimate_host(self.handle, _host_ptr(y), _host_ptr(x), _host_ptr(out), T, M, K, soi_ptr,
+                         _stream_ptr(stream))
+        return out
+
+    def launch_count(self) -> int:
+        return ce_launch_count(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            ce_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _host_ptr(a) -> int:
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"] or a.dtype != np.complex64:
+            raise ValueError("host arrays must be C-contiguous complex64")
+        return a.ctypes.data
+    # torch CPU tensor (possibly pinned)
+    if a.is_cuda or not a.is_contiguous():
+        raise ValueError("host tensors must be contiguous CPU tensors")
+    return a.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return 0
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream

@@ -1,0 +1,408 @@
+// libce host side: parameter validation, window geometry, handle/memory management,
+// launch selection and the host-buffer (end-to-end) pipeline.  See include/ce.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ce_internal.h"
+
+namespace ce {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+
+// Reading A7; generalises PAPER.md:242-257 (Table II edge clamping).
+bool window_table(int32_t N, int32_t b, int32_t s, std::vector<Window> *out) {
+  if (N < 1 || b < 1 || b > N || s < 1 || s > b) return false;
+  const int64_t n_win = (int64_t(N - b) + s - 1) / s + 1;
+  const int32_t m_l = (b - s) / 2;
+  out->clear();
+  out->reserve(size_t(n_win));
+  for (int64_t w = 0; w < n_win; ++w) {
+    Window g;
+    g.a = int32_t(std::min<int64_t>(w * s, N - b));
+    g.o = (w == 0) ? 0 : int32_t(w * s + m_l);
+    g.o_next = (w == n_win - 1) ? N : int32_t((w + 1) * s + m_l);
+    out->push_back(g);
+  }
+  return true;
+}
+
+}  // namespace ce
+
+using ce::set_last_error;
+
+struct ce_handle {
+  int device = -1;
+  int32_t N = 0, b = 0, stride = 0, n_sets = 0, n_win = 0, max_kept = 0;
+  int32_t kernel = CE_KERNEL_AUTO;
+  bool built = false;
+  std::vector<ce::Window> geo;
+  // device
+  double2 *d_r = nullptr;       // [n_sets][b] first column of R_hh (only d < b is needed)
+  double *d_sigma2 = nullptr;   // [n_sets]
+  ce::Window *d_geo = nullptr;  // [n_win]
+  double2 *d_ws = nullptr;      // [n_sets][b(b+1)/2] packed Cholesky factor (FP64)
+  float2 *d_W = nullptr;        // [n_sets][b][b]
+  float2 *d_Wt = nullptr;       // [n_sets][b][b] transposed
+  int32_t *d_flag = nullptr;    // [1] build error flag
+  int32_t *h_flag = nullptr;    // pinned mirror
+  // host-buffer path (grown on demand)
+  void *d_stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done[2] = {nullptr, nullptr};
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int fail(int status, const std::string &msg) {
+  set_last_error(msg);
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  set_last_error(m);
+  return e == cudaErrorMemoryAllocation ? CE_ENOMEM : CE_ECUDA;
+}
+
+#define CE_CUDA(call, what)                    \
+  do {                                         \
+    cudaError_t _e = (call);                   \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+void release(ce_handle *h) {
+  cudaFree(h->d_r);
+  cudaFree(h->d_sigma2);
+  cudaFree(h->d_geo);
+  cudaFree(h->d_ws);
+  cudaFree(h->d_W);
+  cudaFree(h->d_Wt);
+  cudaFree(h->d_flag);
+  cudaFreeHost(h->h_flag);
+  cudaFree(h->d_stage);
+  for (auto &s : h->streams)
+    if (s) cudaStreamDestroy(s);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->ev_x) cudaEventDestroy(h->ev_x);
+  for (auto &e : h->ev_done)
+    if (e) cudaEventDestroy(e);
+}
+
+bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+  auto pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+  return pa < pb + nb && pb < pa + na;
+}
+
+int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
+  if (T < 1 || M < 1 || K < 1)
+    return fail(CE_EINVAL, "T, M and K must be >= 1");
+  // 64-bit element count; the kernels index with 64-bit offsets.
+  const long double elems = (long double)T * M * K * h->N;
+  if (elems > 4.0e12L) return fail(CE_EINVAL, "problem too large");
+  return CE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ce_version(void) { return "libce 0.1 sm_100a (K1 fp64 cholesky, K2 fp32 simt)"; }
+
+const char *ce_status_string(int status) {
+  switch (status) {
+    case CE_OK: return "CE_OK: success";
+    case CE_EINVAL: return "CE_EINVAL: invalid argument";
+    case CE_ENOMEM: return "CE_ENOMEM: out of memory";
+    case CE_ECUDA: return "CE_ECUDA: CUDA runtime error";
+    case CE_ENOTPD: return "CE_ENOTPD: R_b + sigma^2 I is not positive definite";
+    case CE_ESTATE: return "CE_ESTATE: filters not built";
+    case CE_ENODEV: return "CE_ENODEV: no compute capability 10.x CUDA device";
+    default: return "unknown ce_status";
+  }
+}
+
+const char *ce_last_error(void) { return ce::g_last_error.c_str(); }
+
+int ce_window_table(int32_t N, int32_t b, int32_t stride, int32_t *out, int32_t capacity) {
+  std::vector<ce::Window> g;
+  if (!ce::window_table(N, b, stride, &g))
+    return fail(CE_EINVAL, "window table: need N >= 1, 1 <= b <= N, 1 <= stride <= b");
+  const int32_t n = int32_t(g.size());
+  if (out == nullptr && capacity == 0) return n;
+  if (out == nullptr || capacity < n) return fail(CE_EINVAL, "window table: capacity too small");
+  for (int32_t w = 0; w < n; ++w) {
+    out[3 * w + 0] = g[w].a;
+    out[3 * w + 1] = g[w].o;
+    out[3 * w + 2] = g[w].o_next;
+  }
+  return n;
+}
+
+int ce_init(const ce_params *p, ce_handle **out) {
+  if (p == nullptr || out == nullptr) return fail(CE_EINVAL, "ce_init: NULL params or out");
+  if (p->N < 1) return fail(CE_EINVAL, "ce_init: N must be >= 1");
+  if (p->b < 1 || p->b > p->N) return fail(CE_EINVAL, "ce_init: need 1 <= b <= N");
+  if (p->stride < 1 || p->stride > p->b) return fail(CE_EINVAL, "ce_init: need 1 <= stride <= b");
+  if (p->n_sets < 1) return fail(CE_EINVAL, "ce_init: n_sets must be >= 1");
+  if (p->r_hh == nullptr || p->sigma2 == nullptr) return fail(CE_EINVAL, "ce_init: NULL r_hh or sigma2");
+  const int32_t N = p->N, b = p->b, S = p->n_sets;
+  for (int32_t s = 0; s < S; ++s) {
+    const double s2 = p->sigma2[s];
+    if (!std::isfinite(s2) || !(s2 > 0.0)) return fail(CE_EINVAL, "ce_init: sigma2 must be finite and > 0");
+    const double *r = p->r_hh + size_t(s) * N * 2;
+    for (int32_t d = 0; d < N; ++d)
+      if (!std::isfinite(r[2 * d]) || !std::isfinite(r[2 * d + 1]))
+        return fail(CE_EINVAL, "ce_init: r_hh must be finite");
+    if (!(r[0] > 0.0) || std::fabs(r[1]) > 1e-9 * r[0])
+      return fail(CE_EINVAL, "ce_init: r[0] must be real and > 0");
+  }
+  std::vector<ce::Window> geo;
+  if (!ce::window_table(N, b, p->stride, &geo)) return fail(CE_EINVAL, "ce_init: bad geometry");
+
+  int dev = -1, ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1 || cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CE_ENODEV, "ce_init: no CUDA device");
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
+    return fail(CE_ENODEV, "ce_init: libce is built for sm_100a (compute capability 10.x)");
+
+  ce_handle *h = new (std::nothrow) ce_handle();
+  if (h == nullptr) return fail(CE_ENOMEM, "ce_init: host allocation");
+  h->device = dev;
+  h->N = N;
+  h->b = b;
+  h->stride = p->stride;
+  h->n_sets = S;
+  h->geo = geo;
+  h->n_win = int32_t(geo.size());
+  for (auto &g : geo) h->max_kept = std::max(h->max_kept, g.o_next - g.o);
+
+  std::vector<double2> r_b(size_t(S) * b);
+  for (int32_t s = 0; s < S; ++s)
+    for (int32_t d = 0; d < b; ++d)
+      r_b[size_t(s) * b + d] = make_double2(p->r_hh[(size_t(s) * N + d) * 2], p->r_hh[(size_t(s) * N + d) * 2 + 1]);
+  const size_t packed = size_t(b) * (b + 1) / 2;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  chk(cudaMalloc(&h->d_r, r_b.size() * sizeof(double2)));
+  chk(cudaMalloc(&h->d_sigma2, size_t(S) * sizeof(double)));
+  chk(cudaMalloc(&h->d_geo, geo.size() * sizeof(ce::Window)));
+  chk(cudaMalloc(&h->d_ws, size_t(S) * packed * sizeof(double2)));
+  chk(cudaMalloc(&h->d_W, size_t(S) * b * b * sizeof(float2)));
+  chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
+  chk(cudaMalloc(&h->d_flag, sizeof(int32_t)));
+  chk(cudaMallocHost(&h->h_flag, sizeof(int32_t)));
+  if (e == cudaSuccess) {
+    chk(cudaMemcpy(h->d_r, r_b.data(), r_b.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(h->d_sigma2, p->sigma2, size_t(S) * sizeof(double), cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(h->d_geo, geo.data(), geo.size() * sizeof(ce::Window), cudaMemcpyHostToDevice));
+  }
+  if (e != cudaSuccess) {
+    int st = cuda_fail(e, "ce_init: device allocation/copy");
+    release(h);
+    delete h;
+    return st;
+  }
+  *out = h;
+  return CE_OK;
+}
+
+int ce_free(ce_handle *h) {
+  if (h == nullptr) return CE_OK;
+  {
+    DeviceGuard g(h->device);
+    release(h);
+  }
+  delete h;
+  return CE_OK;
+}
+
+int ce_set_kernel(ce_handle *h, int32_t kernel) {
+  if (h == nullptr) return fail(CE_EINVAL, "ce_set_kernel: NULL handle");
+  if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT)
+    return fail(CE_EINVAL, "ce_set_kernel: unknown or unavailable kernel");
+  h->kernel = kernel;
+  return CE_OK;
+}
+
+int ce_launch_count(const ce_handle *h, int64_t *out) {
+  if (h == nullptr || out == nullptr) return fail(CE_EINVAL, "ce_launch_count: NULL argument");
+  *out = h->launches;
+  return CE_OK;
+}
+
+int ce_build_filters(ce_handle *h, void *stream) {
+  if (h == nullptr) return fail(CE_EINVAL, "ce_build_filters: NULL handle");
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(CE_ECUDA, "ce_build_filters: cannot select the handle's device");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->built = false;
+  CE_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(int32_t), st), "ce_build_filters: memset flag");
+  CE_CUDA(ce::launch_filter_build(h->d_r, h->d_sigma2, h->N, h->b, h->n_sets, h->d_ws, h->d_W, h->d_Wt,
+                                  h->d_flag, st, &h->launches),
+          "ce_build_filters: launch");
+  CE_CUDA(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st),
+          "ce_build_filters: flag copy");
+  CE_CUDA(cudaStreamSynchronize(st), "ce_build_filters: synchronize");
+  if (*h->h_flag != 0)
+    return fail(CE_ENOTPD, "ce_build_filters: Cholesky pivot <= 0 or not finite (R_b + sigma^2 I not PD)");
+  h->built = true;
+  return CE_OK;
+}
+
+int ce_get_filters(ce_handle *h, void *host_W) {
+  if (h == nullptr || host_W == nullptr) return fail(CE_EINVAL, "ce_get_filters: NULL argument");
+  if (!h->built) return fail(CE_ESTATE, "ce_get_filters: filters not built");
+  DeviceGuard g(h->device);
+  CE_CUDA(cudaMemcpy(host_W, h->d_W, size_t(h->n_sets) * h->b * h->b * sizeof(float2), cudaMemcpyDeviceToHost),
+          "ce_get_filters: copy");
+  return CE_OK;
+}
+
+static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float2 *out, int32_t T, int32_t M,
+                           int32_t K, const int32_t *soi, cudaStream_t st) {
+  ce::ContractArgs a;
+  a.y = y;
+  a.x = x;
+  a.h = out;
+  a.Wt = h->d_Wt;
+  a.geo = h->d_geo;
+  a.soi = soi;
+  a.T = T;
+  a.M = M;
+  a.K = K;
+  a.N = h->N;
+  a.b = h->b;
+  a.n_win = h->n_win;
+  a.n_sets = h->n_sets;
+  a.max_kept = h->max_kept;
+  cudaError_t e = ce::launch_contract_simt(a, st, &h->launches);
+  if (e != cudaSuccess) return cuda_fail(e, "ce_estimate: kernel launch");
+  return CE_OK;
+}
+
+int ce_estimate(ce_handle *h, const void *d_y, const void *d_x, void *d_h, int32_t T, int32_t M, int32_t K,
+                const int32_t *d_set_of_instance, void *stream) {
+  if (h == nullptr) return fail(CE_EINVAL, "ce_estimate: NULL handle");
+  if (!h->built) return fail(CE_ESTATE, "ce_estimate: call ce_build_filters first");
+  if (d_y == nullptr || d_x == nullptr || d_h == nullptr) return fail(CE_EINVAL, "ce_estimate: NULL pointer");
+  int st = check_sizes(h, T, M, K);
+  if (st != CE_OK) return st;
+  if ((reinterpret_cast<uintptr_t>(d_y) | reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_h)) & 7u)
+    return fail(CE_EINVAL, "ce_estimate: pointers must be 8-byte aligned (complex64)");
+  const size_t ny = size_t(T) * M * K * h->N * sizeof(float2);
+  const size_t nx = size_t(T) * K * h->N * sizeof(float2);
+  if (overlaps(d_h, ny, d_y, ny) || overlaps(d_h, ny, d_x, nx))
+    return fail(CE_EINVAL, "ce_estimate: output aliases an input");
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(CE_ECUDA, "ce_estimate: cannot select the handle's device");
+  return launch_contract(h, static_cast<const float2 *>(d_y), static_cast<const float2 *>(d_x),
+                         static_cast<float2 *>(d_h), T, M, K, d_set_of_instance, static_cast<cudaStream_t>(stream));
+}
+
+int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void *h_host, int32_t T, int32_t M,
+                     int32_t K, const int32_t *set_of_instance, void *stream) {
+  if (h == nullptr) return fail(CE_EINVAL, "ce_estimate_host: NULL handle");
+  if (!h->built) return fail(CE_ESTATE, "ce_estimate_host: call ce_build_filters first");
+  if (y_host == nullptr || x_host == nullptr || h_host == nullptr)
+    return fail(CE_EINVAL, "ce_estimate_host: NULL pointer");
+  int st = check_sizes(h, T, M, K);
+  if (st != CE_OK) return st;
+  const size_t N = size_t(h->N);
+  const size_t ny = size_t(T) * M * K * N * sizeof(float2);
+  const size_t nx = size_t(T) * K * N * sizeof(float2);
+  if (overlaps(h_host, ny, y_host, ny) || overlaps(h_host, ny, x_host, nx))
+    return fail(CE_EINVAL, "ce_estimate_host: output aliases an input");
+  if (set_of_instance)
+    for (int32_t t = 0; t < T; ++t)
+      if (set_of_instance[t] < 0 || set_of_instance[t] >= h->n_sets)
+        return fail(CE_EINVAL, "ce_estimate_host: set_of_instance out of range");
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(CE_ECUDA, "ce_estimate_host: cannot select the handle's device");
+
+  // Device staging: [y | h | x | soi], each 256-byte aligned, grown on demand.
+  auto al = [](size_t n) { return (n + 255) & ~size_t(255); };
+  const size_t need = al(ny) * 2 + al(nx) + al(size_t(T) * sizeof(int32_t));
+  if (need > h->stage_bytes) {
+    cudaFree(h->d_stage);
+    h->d_stage = nullptr;
+    h->stage_bytes = 0;
+    CE_CUDA(cudaMalloc(&h->d_stage, need), "ce_estimate_host: staging allocation");
+    h->stage_bytes = need;
+  }
+  if (h->streams[0] == nullptr) {
+    for (auto &s : h->streams) CE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    CE_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event create");
+    CE_CUDA(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming), "event create");
+    for (auto &e : h->ev_done) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+  }
+  char *base = static_cast<char *>(h->d_stage);
+  float2 *dy = reinterpret_cast<float2 *>(base);
+  float2 *dh = reinterpret_cast<float2 *>(base + al(ny));
+  float2 *dx = reinterpret_cast<float2 *>(base + 2 * al(ny));
+  int32_t *dsoi = reinterpret_cast<int32_t *>(base + 2 * al(ny) + al(nx));
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  // order after prior work on the user's stream
+  CE_CUDA(cudaEventRecord(h->ev_start, user), "event record");
+  CE_CUDA(cudaStreamWaitEvent(h->streams[0], h->ev_start, 0), "stream wait");
+  CE_CUDA(cudaStreamWaitEvent(h->streams[1], h->ev_start, 0), "stream wait");
+  CE_CUDA(cudaMemcpyAsync(dx, x_host, nx, cudaMemcpyHostToDevice, h->streams[0]), "x copy");
+  if (set_of_instance)
+    CE_CUDA(cudaMemcpyAsync(dsoi, set_of_instance, size_t(T) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                            h->streams[0]), "soi copy");
+  CE_CUDA(cudaEventRecord(h->ev_x, h->streams[0]), "event record");
+  CE_CUDA(cudaStreamWaitEvent(h->streams[1], h->ev_x, 0), "stream wait");
+
+  // Chunks of ~4 MB of y: (instance t, antenna range) pairs, alternating streams so the
+  // H2D of chunk i+1 and the D2H of chunk i-1 overlap the kernel of chunk i.
+  const size_t ant_bytes = size_t(K) * N * sizeof(float2);
+  int32_t m_chunk = int32_t(std::max<size_t>(1, (size_t(4) << 20) / ant_bytes));
+  m_chunk = std::min(m_chunk, M);
+  int c = 0;
+  for (int32_t t = 0; t < T; ++t) {
+    for (int32_t m0 = 0; m0 < M; m0 += m_chunk, ++c) {
+      const int32_t mc = std::min(m_chunk, M - m0);
+      const size_t off = (size_t(t) * M + m0) * K * N;
+      const size_t bytes = size_t(mc) * ant_bytes;
+      cudaStream_t s = h->streams[c & 1];
+      CE_CUDA(cudaMemcpyAsync(dy + off, static_cast<const float2 *>(y_host) + off, bytes, cudaMemcpyHostToDevice, s),
+              "y copy");
+      int r = launch_contract(h, dy + off, dx + size_t(t) * K * N, dh + off, 1, mc, K,
+                              set_of_instance ? dsoi + t : nullptr, s);
+      if (r != CE_OK) return r;
+      CE_CUDA(cudaMemcpyAsync(static_cast<float2 *>(h_host) + off, dh + off, bytes, cudaMemcpyDeviceToHost, s),
+              "h copy");
+    }
+  }
+  for (int i = 0; i < 2; ++i) CE_CUDA(cudaEventRecord(h->ev_done[i], h->streams[i]), "event record");
+  for (int i = 0; i < 2; ++i) CE_CUDA(cudaStreamWaitEvent(user, h->ev_done[i], 0), "stream wait");
+  CE_CUDA(cudaStreamSynchronize(user), "ce_estimate_host: synchronize");
+  return CE_OK;
+}
+
+}  // extern "C"

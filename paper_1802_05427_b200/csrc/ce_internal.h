@@ -1,0 +1,46 @@
+// Internal declarations shared by the libce translation units (host API, K1, K2, K3).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ce.h"
+
+namespace ce {
+
+// One window of the geometry table (reading A7).
+struct Window {
+  int32_t a;       // first LS tone read
+  int32_t o;       // first output tone kept
+  int32_t o_next;  // one past the last output tone kept
+};
+
+// Host-side window table; returns false for invalid sizes.
+bool window_table(int32_t N, int32_t b, int32_t s, std::vector<Window> *out);
+
+// Arguments of one contraction launch (K2 / K3).
+struct ContractArgs {
+  const float2 *y;         // [T][M][K][N]
+  const float2 *x;         // [T][K][N]
+  float2 *h;               // [T][M][K][N]
+  const float2 *Wt;        // [n_sets][b][b] transposed filters: Wt[s][j][i] = W[s][i][j]
+  const Window *geo;       // [n_win] (device)
+  const int32_t *soi;      // [T] device or nullptr
+  int32_t T, M, K, N, b, n_win, n_sets, max_kept;
+};
+
+// K1: filter build.  Returns cudaError_t of the launches.
+cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int32_t N, int32_t b,
+                                int32_t n_sets, double2 *d_ws, float2 *d_W, float2 *d_Wt,
+                                int32_t *d_flag, cudaStream_t stream,
+                                int64_t *launches);
+
+// K2: FP32 SIMT contraction.
+cudaError_t launch_contract_simt(const ContractArgs &a, cudaStream_t stream, int64_t *launches);
+
+void set_last_error(const std::string &msg);
+
+}  // namespace ce

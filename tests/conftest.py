@@ -8,9 +8,22 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _load_build():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_ce_build", os.path.join(ROOT, "paper_1802_05427_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; parity tests through the C-ABI")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    # libce.so is git-ignored: (re)build it in-tree if missing or stale (nvcc cross-compiles).
+    _b = _load_build()
+    if not _b.up_to_date():
+        _b.build()
 
 
 def _cuda_available():

@@ -1,0 +1,229 @@
+"""GPU parity: libce (through the C-ABI) vs the complex128 CPU oracle on the same seeded inputs.
+
+Bar (north_star): relative Frobenius error <= 1e-4 per instance t.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from workload import CONFIGS
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _ce():
+    import paper_1802_05427_b200 as ce
+    return ce
+
+
+def _run(N, b, s, r, s2, y, x, soi=None, kernel=None):
+    ce = _ce()
+    est = ce.ChannelEstimator(N, b, s, r, s2)
+    if kernel is not None:
+        ce.ce_set_kernel(est.handle, kernel)
+    est.build()
+    soi_t = None if soi is None else torch.from_numpy(np.ascontiguousarray(soi, np.int32)).cuda()
+    h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), set_of_instance=soi_t)
+    torch.cuda.synchronize()
+    out = h.cpu().numpy()
+    est.close()
+    return out
+
+
+def _inputs(cfg, m_hi=None):
+    r, s2 = workload.channel_stats(cfg, 0)
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x, m_hi=m_hi)
+    return r, s2, x, y, workload.set_of_instance(cfg)
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_config_parity_full(cfg_id):
+    cfg = CONFIGS[cfg_id]
+    r, s2, x, y, soi = _inputs(cfg)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi)
+    ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
+    err = oracle.rel_fro_error_per_instance(h, ref)
+    assert np.all(err <= TOL), err
+    assert np.isfinite(h).all()
+
+
+def test_config4_parity_antenna_subset():
+    """Config 4 (b=150, stride 100, 20 per-slot sets, T=40) on antennas [0,16): the generator is
+    per-(t,m) seeded, so these are exactly the full run's first 16 antennas."""
+    cfg = CONFIGS[4]
+    r, s2, x, y, soi = _inputs(cfg, m_hi=16)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi)
+    ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
+    err = oracle.rel_fro_error_per_instance(h, ref)
+    assert np.all(err <= TOL), err
+
+
+@pytest.mark.parametrize("cfg_id", [4, 5])
+def test_full_size_sampled(cfg_id):
+    """Full BASELINE sizes in one launch; sampled (t, m) slices checked against the oracle."""
+    cfg = CONFIGS[cfg_id]
+    ce = _ce()
+    r, s2 = workload.channel_stats(cfg, 0)
+    soi = workload.set_of_instance(cfg)
+    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2).build()
+    x = workload.gen_pilots(cfg, 0)
+    y_d = torch.empty((cfg.T, cfg.M, cfg.K, cfg.N), dtype=torch.complex64, device="cuda")
+    step = 8
+    for t in range(cfg.T):                       # generate on host per instance, upload
+        for m0 in range(0, cfg.M, 64):
+            y_d[t, m0:m0 + 64] = torch.from_numpy(
+                workload.gen_instances(cfg, 0, t_lo=t, t_hi=t + 1, m_lo=m0, m_hi=min(cfg.M, m0 + 64),
+                                       x=x[t:t + 1])[0]).cuda()
+    x_d = torch.from_numpy(x).cuda()
+    h = est.estimate(y_d, x_d, set_of_instance=torch.from_numpy(soi).cuda())
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    for t in rng.choice(cfg.T, size=min(cfg.T, 4), replace=False):
+        for m in rng.choice(cfg.M, size=3, replace=False):
+            y_tm = y_d[t, m:m + 1].cpu().numpy()[None]
+            ref = oracle.block_lmmse(y_tm, x[t:t + 1], r, s2, soi[t:t + 1], cfg.b, cfg.stride)
+            got = h[t, m:m + 1].cpu().numpy()[None]
+            assert oracle.rel_fro_error_per_instance(got, ref)[0] <= TOL, (t, m)
+    # properties at full size: finite everywhere, output energy ~ channel energy (sum p = 1)
+    assert torch.isfinite(torch.view_as_real(h)).all()
+    p = (h.abs() ** 2).mean().item()
+    assert 0.5 < p < 1.5, p
+    del y_d, h
+    est.close()
+    _ = step
+
+
+@pytest.mark.parametrize("N,b,s,M,K,T", [
+    (37, 13, 4, 3, 5, 2),      # ragged everything, odd overlap, clamped last window
+    (96, 96, 96, 2, 3, 1),     # b = N: full LMMSE
+    (40, 1, 1, 4, 2, 1),       # b = 1: scalar Wiener
+    (40, 8, 1, 5, 3, 2),       # stride 1: maximal overlap
+    (300, 256, 44, 2, 2, 1),   # large b: K1 Cholesky in global memory, > 3 K2 row tiles
+    (130, 65, 64, 11, 7, 3),   # cols = 77 spans two column tiles with a ragged tail
+])
+def test_edge_shapes(N, b, s, M, K, T):
+    rng = np.random.default_rng(N * 7 + b)
+    L = 5
+    p = np.exp(-np.arange(L) / 2.0)
+    p /= p.sum()
+    tau = np.array([0.0, 1.3, 2.0, 4.7, 6.1])
+    d = np.arange(N)
+    r = (p[None] * np.exp(-2j * np.pi * np.outer(d, tau) / (2 * N))).sum(1)[None]
+    s2 = np.array([0.05])
+    y = (rng.standard_normal((T, M, K, N)) + 1j * rng.standard_normal((T, M, K, N))).astype(np.complex64)
+    x = np.exp(2j * np.pi * rng.random((T, K, N))).astype(np.complex64) * np.float32(1.7)  # non-unit pilots
+    h = _run(N, b, s, r, s2, y, x)
+    ref = oracle.block_lmmse(y, x, r, s2, None, b, s)
+    assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL)
+    if b == N:
+        full = oracle.full_lmmse(y, x, r, s2, None)
+        assert np.all(oracle.rel_fro_error_per_instance(h, full) <= TOL)
+
+
+def test_filters_match_oracle():
+    ce = _ce()
+    for cfg_id in (1, 2, 3, 4, 5):
+        cfg = CONFIGS[cfg_id]
+        r, s2 = workload.channel_stats(cfg, 0)
+        est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2).build()
+        W = est.filters()
+        for st in range(cfg.n_sets):
+            ref = oracle.block_filter(r[st], s2[st], cfg.b)
+            rel = np.linalg.norm(W[st] - ref) / np.linalg.norm(ref)
+            assert rel < 2e-7, (cfg_id, st, rel)      # FP64 build, complex64 rounding only
+        est.close()
+
+
+def test_not_positive_definite_and_state():
+    ce = _ce()
+    N = 16
+    r = np.zeros((1, N), np.complex128)
+    r[0, 0], r[0, 1] = 1.0, 2.0              # |r_1| > r_0: R_b indefinite
+    est = ce.ChannelEstimator(N, 8, 8, r, [1e-3])
+    with pytest.raises(ce.CEError) as e:
+        est.build()
+    assert e.value.status == ce.CE_ENOTPD
+    y = torch.zeros((1, 1, 1, N), dtype=torch.complex64, device="cuda")
+    x = torch.ones((1, 1, N), dtype=torch.complex64, device="cuda")
+    with pytest.raises(ce.CEError) as e:
+        est.estimate(y, x)
+    assert e.value.status == ce.CE_ESTATE
+    est.close()
+
+
+def _cfg2_estimator():
+    ce = _ce()
+    cfg = CONFIGS[2]
+    r, s2, x, y, soi = _inputs(cfg)
+    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2).build()
+    return ce, cfg, est, r, s2, x, y, soi
+
+
+def test_shard_invariance_determinism_and_host_path():
+    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator()
+    y_d, x_d = torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda()
+    soi_d = torch.from_numpy(soi).cuda()
+    full = est.estimate(y_d, x_d, set_of_instance=soi_d)
+    again = est.estimate(y_d, x_d, set_of_instance=soi_d)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(full), torch.view_as_real(again))      # deterministic
+    # antenna shards through offset device pointers (G = 1, 2, 4, 8 on one device)
+    for G in (2, 4, 8):
+        out = torch.empty_like(y_d)
+        Mg = cfg.M // G
+        for t in range(cfg.T):
+            for g in range(G):
+                ce.ce_estimate(est.handle, y_d[t, g * Mg].data_ptr(), x_d[t].data_ptr(), out[t, g * Mg].data_ptr(),
+                               1, Mg, cfg.K, soi_d[t:].data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.view_as_real(out), torch.view_as_real(full)), G
+    # host-buffer end-to-end entry point gives the same bits
+    h_host = est.estimate_host(y, x, set_of_instance=soi)
+    assert np.array_equal(h_host.view(np.float32), full.cpu().numpy().view(np.float32))
+    pinned_y = torch.from_numpy(y).pin_memory()
+    pinned_out = torch.empty(y.shape, dtype=torch.complex64).pin_memory()
+    est.estimate_host(pinned_y, torch.from_numpy(x), out=pinned_out, set_of_instance=soi)
+    assert torch.equal(torch.view_as_real(pinned_out), torch.view_as_real(full.cpu()))
+    est.close()
+
+
+def test_zero_linearity_bad_set_and_validation():
+    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator()
+    x_d = torch.from_numpy(x).cuda()
+    soi_d = torch.from_numpy(soi).cuda()
+    z = est.estimate(torch.zeros(y.shape, dtype=torch.complex64, device="cuda"), x_d, set_of_instance=soi_d)
+    assert not torch.view_as_real(z).any()
+    # out-of-range set index -> that instance is NaN, the other instance is untouched
+    bad = torch.tensor([0, 5], dtype=torch.int32, device="cuda")
+    hb = est.estimate(torch.from_numpy(y).cuda(), x_d, set_of_instance=bad).cpu().numpy()
+    assert np.isnan(hb[1]).all() and np.isfinite(hb[0]).all()
+    # aliasing and misalignment are rejected
+    y_d = torch.from_numpy(y).cuda()
+    lib = ce.ce.lib
+    st = lib.ce_estimate(est.handle, y_d.data_ptr(), x_d.data_ptr(), y_d.data_ptr(), cfg.T, cfg.M, cfg.K, None, None)
+    assert st == ce.CE_EINVAL
+    st = lib.ce_estimate(est.handle, y_d.data_ptr() + 4, x_d.data_ptr(), y_d.data_ptr() + 4, 1, 1, 1, None, None)
+    assert st == ce.CE_EINVAL
+    st = lib.ce_estimate(est.handle, y_d.data_ptr(), x_d.data_ptr(), y_d.data_ptr(), 0, cfg.M, cfg.K, None, None)
+    assert st == ce.CE_EINVAL
+    assert est.launch_count() >= 3
+    est.close()
+
+
+def test_mse_gain_on_gpu():
+    """End-to-end sanity on config 3: GPU estimate MSE vs the true channel matches the closed form."""
+    cfg = dataclasses.replace(CONFIGS[3], M=64)
+    r, s2 = workload.channel_stats(cfg, 0)
+    x = workload.gen_pilots(cfg, 0)
+    y, H = workload.gen_instances(cfg, 0, x=x, return_channel=True)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x)
+    mse = np.mean(np.abs(h - H) ** 2)
+    cf = oracle.block_mse(r[0], s2[0], cfg.b)
+    assert abs(mse / cf - 1) < 0.05
