@@ -33,13 +33,21 @@ __device__ __forceinline__ float2 ls_div(float2 y, float2 x) {
 }
 
 struct Tile {
-  float2 a[4];  // A prefetch: 4 elements per thread
-  float2 w[4];  // W prefetch
+  float2 y[4];  // raw y prefetch (LS applied at stash time, after the compute phase)
+  float2 x[4];  // matching pilots
+  float2 w[4];  // W^T prefetch
+};
+
+union __align__(16) Smem {
+  struct {
+    float2 As[2][BM][AS];
+    float2 Ws[2][BK][BN];
+  } k;
+  float2 Cs[BM][BN + 1];  // output staging for coalesced row stores
 };
 
 __global__ void __launch_bounds__(NT, 2) k2_simt(ContractArgs p, int row_tiles) {
-  __shared__ __align__(16) float2 As[2][BM][AS];
-  __shared__ __align__(16) float2 Ws[2][BK][BN];
+  __shared__ Smem sm;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lc = lane & 7, lr = lane >> 3, wc = warp & 1, wr = warp >> 1;
@@ -59,14 +67,24 @@ __global__ void __launch_bounds__(NT, 2) k2_simt(ContractArgs p, int row_tiles) 
   // load mapping
   const int a_kk = tid & 15, a_c = tid >> 4;   // A: 16 tones x 16 columns per pass, 4 passes
   const int w_r = tid & 63, w_kk = tid >> 6;   // W: 64 rows x 4 tones per pass, 4 passes
+  size_t y_off[4], x_off[4];
+  bool c_ok[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + a_c + 16 * q;
+    c_ok[q] = c < cols;
+    y_off[q] = size_t(c) * N;
+    x_off[q] = size_t(c_ok[q] ? c % p.K : 0) * N;
+  }
 
   for (int t = blockIdx.z; t < p.T; t += gridDim.z) {
     const int set = p.soi ? p.soi[t] : 0;
     const size_t y_inst = size_t(t) * cols * N;
     if (set < 0 || set >= p.n_sets) {  // documented: out-of-range set -> NaN outputs
+      const float qnan = __int_as_float(0x7fc00000);
       for (int e = tid; e < BM * rows; e += NT) {
         const int c = c0 + e / rows, i = e % rows;
-        if (c < cols) p.h[y_inst + size_t(c) * N + g.o + r_base + i] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+        if (c < cols) p.h[y_inst + size_t(c) * N + g.o + r_base + i] = make_float2(qnan, qnan);
       }
       continue;
     }
@@ -75,26 +93,28 @@ __global__ void __launch_bounds__(NT, 2) k2_simt(ContractArgs p, int row_tiles) 
     const float2 *__restrict__ xb = p.x + size_t(t) * p.K * N + g.a;
 
     auto fetch = [&](int k0, Tile &f) {
+      const int k = k0 + a_kk;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int c = c0 + a_c + 16 * q, k = k0 + a_kk;
-        float2 v = make_float2(0.f, 0.f);
-        if (c < cols && k < b) v = ls_div(__ldg(yb + size_t(c) * N + k), __ldg(xb + size_t(c % p.K) * N + k));
-        f.a[q] = v;
+        f.y[q] = make_float2(0.f, 0.f);
+        f.x[q] = make_float2(1.f, 0.f);
+        if (c_ok[q] && k < b) {
+          f.y[q] = __ldg(yb + y_off[q] + k);
+          f.x[q] = __ldg(xb + x_off[q] + k);
+        }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int k = k0 + w_kk + 4 * q;
-        float2 v = make_float2(0.f, 0.f);
-        if (w_r < rows && k < b) v = __ldg(Wt + size_t(k) * b + row0 + w_r);
-        f.w[q] = v;
+        const int kw = k0 + w_kk + 4 * q;
+        f.w[q] = make_float2(0.f, 0.f);
+        if (w_r < rows && kw < b) f.w[q] = __ldg(Wt + size_t(kw) * b + row0 + w_r);
       }
     };
     auto stash = [&](int buf, const Tile &f) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) As[buf][a_c + 16 * q][a_kk] = f.a[q];
+      for (int q = 0; q < 4; ++q) sm.k.As[buf][a_c + 16 * q][a_kk] = ls_div(f.y[q], f.x[q]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) Ws[buf][w_kk + 4 * q][w_r] = f.w[q];
+      for (int q = 0; q < 4; ++q) sm.k.Ws[buf][w_kk + 4 * q][w_r] = f.w[q];
     };
 
     float acc[4][4][2];
@@ -105,30 +125,31 @@ __global__ void __launch_bounds__(NT, 2) k2_simt(ContractArgs p, int row_tiles) 
 
     Tile f;
     fetch(0, f);
-    __syncthreads();  // previous instance's readers are done with buffer 0
+    __syncthreads();  // previous instance's readers are done with the shared buffers
     stash(0, f);
     __syncthreads();
     for (int kc = 0; kc < nk; ++kc) {
       const int buf = kc & 1;
+      const int klim = b - kc * BK;  // >= BK except in the last chunk
       if (kc + 1 < nk) fetch((kc + 1) * BK, f);
       if (warp_active) {
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 2) {
+          if (kk >= klim) break;  // warp-uniform: skip the zero padding of the K tail
           float4 av[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            av[i] = *reinterpret_cast<const float4 *>(&As[buf][wc * 32 + lc + 8 * i][kk]);
+            av[i] = *reinterpret_cast<const float4 *>(&sm.k.As[buf][wc * 32 + lc + 8 * i][kk]);
           float4 wv0[2], wv1[2];
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
-            wv0[jj] = *reinterpret_cast<const float4 *>(&Ws[buf][kk][wr * 16 + lr * 4 + 2 * jj]);
-            wv1[jj] = *reinterpret_cast<const float4 *>(&Ws[buf][kk + 1][wr * 16 + lr * 4 + 2 * jj]);
+            wv0[jj] = *reinterpret_cast<const float4 *>(&sm.k.Ws[buf][kk][wr * 16 + lr * 4 + 2 * jj]);
+            wv1[jj] = *reinterpret_cast<const float4 *>(&sm.k.Ws[buf][kk + 1][wr * 16 + lr * 4 + 2 * jj]);
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              // k = kk: A = (av.x, av.y), W row j = wv0[j/2].{xy|zw}
               const float wr0 = (j & 1) ? wv0[j >> 1].z : wv0[j >> 1].x;
               const float wi0 = (j & 1) ? wv0[j >> 1].w : wv0[j >> 1].y;
               const float wr1 = (j & 1) ? wv1[j >> 1].z : wv1[j >> 1].x;
@@ -151,18 +172,21 @@ __global__ void __launch_bounds__(NT, 2) k2_simt(ContractArgs p, int row_tiles) 
       }
     }
 
+    // stage the 64 x 64 tile in shared memory, then write each column's kept rows contiguously
+    __syncthreads();
     if (warp_active) {
-      float2 *hb = p.h + y_inst + g.o + r_base;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = c0 + wc * 32 + lc + 8 * i;
-        if (c >= cols) continue;
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = wr * 16 + lr * 4 + j;
-          if (r < rows) hb[size_t(c) * N + r] = make_float2(acc[i][j][0], acc[i][j][1]);
-        }
-      }
+        for (int j = 0; j < 4; ++j)
+          sm.Cs[wc * 32 + lc + 8 * i][wr * 16 + lr * 4 + j] = make_float2(acc[i][j][0], acc[i][j][1]);
+    }
+    __syncthreads();
+    float2 *hb = p.h + y_inst + g.o + r_base;
+    for (int cc = warp; cc < BM; cc += NT / 32) {
+      const int c = c0 + cc;
+      if (c >= cols) break;
+      for (int r = lane; r < rows; r += 32) hb[size_t(c) * N + r] = sm.Cs[cc][r];
     }
   }
 }
