@@ -274,19 +274,37 @@ def run_ours(args, cfg):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * E * e2e_steps / (float(e2e_ms.item()) * 1e-3)
 
-    # roofline of the dominant kernel (the contraction): 8b flops per estimate, FP32 SIMT peak
+    # roofline of the dominant kernel (the contraction, one launch per step)
     props = torch.cuda.get_device_properties(dev)
     peaks = _peaks()
+    sel = est.selected_kernel()
     sm_max = peaks.get("sm_max_mhz") or clk.summary().get("sm_max_mhz") or 1965.0
     fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6     # FFMA lanes x 2 flops x clock
-    flops = 8.0 * cfg.b * E
-    achieved = flops / kernel_s
-    traffic = _ncu_traffic("k2_simt")
-    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak, "traffic": traffic,
-            "kernel": "k2_simt", "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz",
-            "algorithmic_bytes_per_launch": 16 * E + 8 * cfg.T * cfg.K * cfg.N,
-            "hbm_frac": (16 * E / kernel_s) / (peaks.get("hbm_gbs", 6548.8) * 1e9)}
+    hbm_bw = peaks.get("hbm_gbs", 6548.8) * 1e9
+    flops = 8.0 * cfg.b * E                                  # 4 real MACs per complex MAC, b per estimate
+    alg_bytes = 16 * E + 8 * cfg.T * cfg.K * cfg.N            # y read + h written + pilots
+    if sel == ce.CE_KERNEL_TF32X3:
+        bf16 = peaks.get("bf16_tflops", 1605.7) * 1e12
+        tc_peak = bf16 * 0.5 / 3.0      # TF32 = 1/2 bf16 (nominal ratio); 3 MMAs per product (hi/lo split)
+        t_tc, t_hbm = flops / tc_peak, alg_bytes / hbm_bw
+        kname = "k3_tf32x3"
+        if t_tc >= t_hbm:
+            roof = {"bound": "tensor", "achieved": flops / kernel_s / 1e12, "peak": tc_peak / 1e12,
+                    "unit": "TFLOP/s", "frac": (flops / kernel_s) / tc_peak,
+                    "peak_source": "MEASURED_PEAKS bf16_tflops x 1/2 (tf32:bf16 nominal) / 3 (3xTF32 MMAs per product)"}
+        else:
+            roof = {"bound": "hbm", "achieved": alg_bytes / kernel_s / 1e9, "peak": hbm_bw / 1e9, "unit": "GB/s",
+                    "frac": (alg_bytes / kernel_s) / hbm_bw, "peak_source": "MEASURED_PEAKS hbm_gbs"}
+        roof["roofline_time_us"] = max(t_tc, t_hbm) * 1e6
+    else:
+        kname = "k2_simt"
+        roof = {"bound": "alu", "achieved": flops / kernel_s / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
+                "frac": (flops / kernel_s) / fp32_peak,
+                "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz",
+                "roofline_time_us": max(flops / fp32_peak, alg_bytes / hbm_bw) * 1e6}
+    roof.update({"traffic": _ncu_traffic(kname), "kernel": kname, "kernel_us": kernel_s * 1e6,
+                 "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
+                 "hbm_frac": (alg_bytes / kernel_s) / hbm_bw, "fp32_simt_frac": (flops / kernel_s) / fp32_peak})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,7 +323,7 @@ def run_ours(args, cfg):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded workload generator, SURVEY.md §8(d) recipe)",
             "config": _cfg_json(cfg, {"l2": f"rotating {nbuf} y/h buffer pairs ({nbuf * step_bytes / 2**20:.0f} MiB > L2)",
-                                      "kernel": {0: "auto", 1: "simt", 2: "tf32x3"}[args.kernel],
+                                      "kernel": {0: "auto", 1: "simt", 2: "tf32x3"}[args.kernel] + f"->{kname}",
                                       "global_batch_instances": world * cfg.T,
                                       "parallelism": f"antenna/batch shard x{world}"}),
             "roofline": roof,

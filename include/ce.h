@@ -118,8 +118,13 @@ int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void 
 /* Free W, workspace, staging buffers and the handle.  NULL is allowed (no-op). */
 int ce_free(ce_handle *h);
 
-/* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value. */
+/* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value, or for
+ * CE_KERNEL_TF32X3 when some window does not fit its tile (2*kept + (2*(o_w-a_w) mod 8) > 256).
+ * CE_KERNEL_AUTO (default) = TF32X3 when it fits, else SIMT; both meet the 1e-4 parity bar. */
 int ce_set_kernel(ce_handle *h, int32_t kernel);
+
+/* The kernel ce_estimate will launch (CE_KERNEL_SIMT or CE_KERNEL_TF32X3) after AUTO resolution. */
+int ce_selected_kernel(const ce_handle *h, int32_t *out);
 
 /* Copy the built filters to host memory: complex64 [n_sets][b][b] row-major (W[i][j] multiplies
  * H_LS[a_w + j] for output a_w + i).  Synchronous.  CE_ESTATE if not built. */

@@ -24,6 +24,7 @@ from .ce import (  # noqa: F401
     ce_init,
     ce_last_error,
     ce_launch_count,
+    ce_selected_kernel,
     ce_set_kernel,
     ce_status_string,
     ce_version,

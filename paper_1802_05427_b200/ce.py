@@ -27,6 +27,7 @@ CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3 = 0, 1, 2
 
 # every function declared in include/ce.h (tests check the .so exports all of them)
 EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+            "ce_selected_kernel",
             "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
             "ce_version")
 
@@ -42,6 +43,7 @@ lib.ce_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_i
 lib.ce_estimate_host.argtypes = lib.ce_estimate.argtypes
 lib.ce_free.argtypes = [c_void_p]
 lib.ce_set_kernel.argtypes = [c_void_p, c_int32]
+lib.ce_selected_kernel.argtypes = [c_void_p, POINTER(c_int32)]
 lib.ce_get_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_window_table.argtypes = [c_int32, c_int32, c_int32, POINTER(c_int32), c_int32]
 lib.ce_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
@@ -52,6 +54,7 @@ lib.ce_last_error.restype = c_char_p
 lib.ce_version.argtypes = []
 lib.ce_version.restype = c_char_p
 for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+           "ce_selected_kernel",
            "ce_get_filters", "ce_window_table", "ce_launch_count"):
     getattr(lib, _n).restype = c_int
 
@@ -138,6 +141,12 @@ def ce_set_kernel(h: int, kernel: int) -> None:
     _check(lib.ce_set_kernel(h, kernel), "ce_set_kernel")
 
 
+def ce_selected_kernel(h: int) -> int:
+    v = c_int32()
+    _check(lib.ce_selected_kernel(h, ctypes.byref(v)), "ce_selected_kernel")
+    return v.value
+
+
 def ce_get_filters(h: int, n_sets: int, b: int) -> np.ndarray:
     out = np.empty((n_sets, b, b), np.complex64)
     _check(lib.ce_get_filters(h, out.ctypes.data), "ce_get_filters")
@@ -205,6 +214,9 @@ class ChannelEstimator:
         ce_estimate_host(self.handle, _host_ptr(y), _host_ptr(x), _host_ptr(out), T, M, K, soi_ptr,
                          _stream_ptr(stream))
         return out
+
+    def selected_kernel(self) -> int:
+        return ce_selected_kernel(self.handle)
 
     def launch_count(self) -> int:
         return ce_launch_count(self.handle)

@@ -51,6 +51,9 @@ struct ce_handle {
   double2 *d_ws = nullptr;      // [n_sets][b(b+1)/2] packed Cholesky factor (FP64)
   float2 *d_W = nullptr;        // [n_sets][b][b]
   float2 *d_Wt = nullptr;       // [n_sets][b][b] transposed
+  float *d_bank = nullptr;      // K3 filter bank: hi plane then lo plane, [n_sets][nkc][NR][32] each
+  size_t bank_plane = 0;        // floats per plane
+  bool tf32_ok = false;         // every window fits the K3 tile (N <= 256)
   int32_t *d_flag = nullptr;    // [1] build error flag
   int32_t *h_flag = nullptr;    // pinned mirror
   // host-buffer path (grown on demand)
@@ -100,6 +103,7 @@ void release(ce_handle *h) {
   cudaFree(h->d_ws);
   cudaFree(h->d_W);
   cudaFree(h->d_Wt);
+  cudaFree(h->d_bank);
   cudaFree(h->d_flag);
   cudaFreeHost(h->h_flag);
   cudaFree(h->d_stage);
@@ -129,7 +133,7 @@ int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
 
 extern "C" {
 
-const char *ce_version(void) { return "libce 0.1 sm_100a (K1 fp64 cholesky, K2 fp32 simt)"; }
+const char *ce_version(void) { return "libce 0.2 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3)"; }
 
 const char *ce_status_string(int status) {
   switch (status) {
@@ -207,6 +211,12 @@ int ce_init(const ce_params *p, ce_handle **out) {
     for (int32_t d = 0; d < b; ++d)
       r_b[size_t(s) * b + d] = make_double2(p->r_hh[(size_t(s) * N + d) * 2], p->r_hh[(size_t(s) * N + d) * 2 + 1]);
   const size_t packed = size_t(b) * (b + 1) / 2;
+  h->tf32_ok = ce::tf32x3_supported(b, geo);
+  if (h->tf32_ok) {
+    int32_t nkc, NR;
+    ce::tf32x3_bank_shape(b, &nkc, &NR);
+    h->bank_plane = size_t(S) * nkc * NR * 32;
+  }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
   chk(cudaMalloc(&h->d_r, r_b.size() * sizeof(double2)));
@@ -215,6 +225,7 @@ int ce_init(const ce_params *p, ce_handle **out) {
   chk(cudaMalloc(&h->d_ws, size_t(S) * packed * sizeof(double2)));
   chk(cudaMalloc(&h->d_W, size_t(S) * b * b * sizeof(float2)));
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
+  if (h->tf32_ok) chk(cudaMalloc(&h->d_bank, 2 * h->bank_plane * sizeof(float)));
   chk(cudaMalloc(&h->d_flag, sizeof(int32_t)));
   chk(cudaMallocHost(&h->h_flag, sizeof(int32_t)));
   if (e == cudaSuccess) {
@@ -244,9 +255,18 @@ int ce_free(ce_handle *h) {
 
 int ce_set_kernel(ce_handle *h, int32_t kernel) {
   if (h == nullptr) return fail(CE_EINVAL, "ce_set_kernel: NULL handle");
-  if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT)
-    return fail(CE_EINVAL, "ce_set_kernel: unknown or unavailable kernel");
+  if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT && kernel != CE_KERNEL_TF32X3)
+    return fail(CE_EINVAL, "ce_set_kernel: unknown kernel");
+  if (kernel == CE_KERNEL_TF32X3 && !h->tf32_ok)
+    return fail(CE_EINVAL, "ce_set_kernel: TF32X3 needs 2*kept + row alignment <= 256 for every window");
   h->kernel = kernel;
+  return CE_OK;
+}
+
+int ce_selected_kernel(const ce_handle *h, int32_t *out) {
+  if (h == nullptr || out == nullptr) return fail(CE_EINVAL, "ce_selected_kernel: NULL argument");
+  *out = (h->kernel == CE_KERNEL_TF32X3 || (h->kernel == CE_KERNEL_AUTO && h->tf32_ok)) ? CE_KERNEL_TF32X3
+                                                                                        : CE_KERNEL_SIMT;
   return CE_OK;
 }
 
@@ -266,6 +286,9 @@ int ce_build_filters(ce_handle *h, void *stream) {
   CE_CUDA(ce::launch_filter_build(h->d_r, h->d_sigma2, h->N, h->b, h->n_sets, h->d_ws, h->d_W, h->d_Wt,
                                   h->d_flag, st, &h->launches),
           "ce_build_filters: launch");
+  if (h->tf32_ok)
+    CE_CUDA(ce::launch_build_bank(h->d_W, h->b, h->n_sets, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches),
+            "ce_build_filters: bank launch");
   CE_CUDA(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st),
           "ce_build_filters: flag copy");
   CE_CUDA(cudaStreamSynchronize(st), "ce_build_filters: synchronize");
@@ -301,7 +324,9 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
   a.n_win = h->n_win;
   a.n_sets = h->n_sets;
   a.max_kept = h->max_kept;
-  cudaError_t e = ce::launch_contract_simt(a, st, &h->launches);
+  const bool use_tc = h->kernel == CE_KERNEL_TF32X3 || (h->kernel == CE_KERNEL_AUTO && h->tf32_ok);
+  cudaError_t e = use_tc ? ce::launch_contract_tf32x3(a, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches)
+                         : ce::launch_contract_simt(a, st, &h->launches);
   if (e != cudaSuccess) return cuda_fail(e, "ce_estimate: kernel launch");
   return CE_OK;
 }

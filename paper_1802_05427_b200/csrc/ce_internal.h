@@ -41,6 +41,14 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
 // K2: FP32 SIMT contraction.
 cudaError_t launch_contract_simt(const ContractArgs &a, cudaStream_t stream, int64_t *launches);
 
+// K3: tcgen05 3xTF32 contraction over the pre-split, pre-swizzled filter bank.
+bool tf32x3_supported(int32_t b, const std::vector<Window> &geo);
+void tf32x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR);
+cudaError_t launch_build_bank(const float2 *d_W, int32_t b, int32_t n_sets, float *bank_hi, float *bank_lo,
+                              cudaStream_t stream, int64_t *launches);
+cudaError_t launch_contract_tf32x3(const ContractArgs &a, const float *bank_hi, const float *bank_lo,
+                                   cudaStream_t stream, int64_t *launches);
+
 void set_last_error(const std::string &msg);
 
 }  // namespace ce

@@ -82,6 +82,7 @@ def test_null_handle_calls():
     assert lib.ce_set_kernel(None, 0) == ce.CE_EINVAL
     assert lib.ce_get_filters(None, None) == ce.CE_EINVAL
     assert lib.ce_launch_count(None, None) == ce.CE_EINVAL
+    assert lib.ce_selected_kernel(None, None) == ce.CE_EINVAL
 
 
 def test_no_device_is_loud():

@@ -22,12 +22,25 @@ def _ce():
     return ce
 
 
-def _run(N, b, s, r, s2, y, x, soi=None, kernel=None):
+KERNELS = [1, 2]          # CE_KERNEL_SIMT (K2), CE_KERNEL_TF32X3 (K3)
+
+
+def _estimator(N, b, s, r, s2, kernel):
     ce = _ce()
     est = ce.ChannelEstimator(N, b, s, r, s2)
     if kernel is not None:
-        ce.ce_set_kernel(est.handle, kernel)
-    est.build()
+        try:
+            ce.ce_set_kernel(est.handle, kernel)
+        except ce.CEError as e:
+            est.close()
+            if e.status == ce.CE_EINVAL and kernel == ce.CE_KERNEL_TF32X3:
+                pytest.skip("window too wide for the K3 tile (2*kept > 256)")
+            raise
+    return est.build()
+
+
+def _run(N, b, s, r, s2, y, x, soi=None, kernel=None):
+    est = _estimator(N, b, s, r, s2, kernel)
     soi_t = None if soi is None else torch.from_numpy(np.ascontiguousarray(soi, np.int32)).cuda()
     h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), set_of_instance=soi_t)
     torch.cuda.synchronize()
@@ -43,39 +56,40 @@ def _inputs(cfg, m_hi=None):
     return r, s2, x, y, workload.set_of_instance(cfg)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("cfg_id", [1, 2, 3])
-def test_config_parity_full(cfg_id):
+def test_config_parity_full(cfg_id, kernel):
     cfg = CONFIGS[cfg_id]
     r, s2, x, y, soi = _inputs(cfg)
-    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
     err = oracle.rel_fro_error_per_instance(h, ref)
     assert np.all(err <= TOL), err
     assert np.isfinite(h).all()
 
 
-def test_config4_parity_antenna_subset():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config4_parity_antenna_subset(kernel):
     """Config 4 (b=150, stride 100, 20 per-slot sets, T=40) on antennas [0,16): the generator is
     per-(t,m) seeded, so these are exactly the full run's first 16 antennas."""
     cfg = CONFIGS[4]
     r, s2, x, y, soi = _inputs(cfg, m_hi=16)
-    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
     err = oracle.rel_fro_error_per_instance(h, ref)
     assert np.all(err <= TOL), err
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("cfg_id", [4, 5])
-def test_full_size_sampled(cfg_id):
+def test_full_size_sampled(cfg_id, kernel):
     """Full BASELINE sizes in one launch; sampled (t, m) slices checked against the oracle."""
     cfg = CONFIGS[cfg_id]
-    ce = _ce()
     r, s2 = workload.channel_stats(cfg, 0)
     soi = workload.set_of_instance(cfg)
-    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2).build()
+    est = _estimator(cfg.N, cfg.b, cfg.stride, r, s2, kernel)
     x = workload.gen_pilots(cfg, 0)
     y_d = torch.empty((cfg.T, cfg.M, cfg.K, cfg.N), dtype=torch.complex64, device="cuda")
-    step = 8
     for t in range(cfg.T):                       # generate on host per instance, upload
         for m0 in range(0, cfg.M, 64):
             y_d[t, m0:m0 + 64] = torch.from_numpy(
@@ -97,9 +111,9 @@ def test_full_size_sampled(cfg_id):
     assert 0.5 < p < 1.5, p
     del y_d, h
     est.close()
-    _ = step
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("N,b,s,M,K,T", [
     (37, 13, 4, 3, 5, 2),      # ragged everything, odd overlap, clamped last window
     (96, 96, 96, 2, 3, 1),     # b = N: full LMMSE
@@ -108,7 +122,7 @@ def test_full_size_sampled(cfg_id):
     (300, 256, 44, 2, 2, 1),   # large b: K1 Cholesky in global memory, > 3 K2 row tiles
     (130, 65, 64, 11, 7, 3),   # cols = 77 spans two column tiles with a ragged tail
 ])
-def test_edge_shapes(N, b, s, M, K, T):
+def test_edge_shapes(N, b, s, M, K, T, kernel):
     rng = np.random.default_rng(N * 7 + b)
     L = 5
     p = np.exp(-np.arange(L) / 2.0)
@@ -119,7 +133,7 @@ def test_edge_shapes(N, b, s, M, K, T):
     s2 = np.array([0.05])
     y = (rng.standard_normal((T, M, K, N)) + 1j * rng.standard_normal((T, M, K, N))).astype(np.complex64)
     x = np.exp(2j * np.pi * rng.random((T, K, N))).astype(np.complex64) * np.float32(1.7)  # non-unit pilots
-    h = _run(N, b, s, r, s2, y, x)
+    h = _run(N, b, s, r, s2, y, x, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, None, b, s)
     assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL)
     if b == N:
@@ -158,16 +172,17 @@ def test_not_positive_definite_and_state():
     est.close()
 
 
-def _cfg2_estimator():
+def _cfg2_estimator(kernel=None):
     ce = _ce()
     cfg = CONFIGS[2]
     r, s2, x, y, soi = _inputs(cfg)
-    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2).build()
+    est = _estimator(cfg.N, cfg.b, cfg.stride, r, s2, kernel)
     return ce, cfg, est, r, s2, x, y, soi
 
 
-def test_shard_invariance_determinism_and_host_path():
-    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator()
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_shard_invariance_determinism_and_host_path(kernel):
+    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator(kernel)
     y_d, x_d = torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda()
     soi_d = torch.from_numpy(soi).cuda()
     full = est.estimate(y_d, x_d, set_of_instance=soi_d)
@@ -194,8 +209,9 @@ def test_shard_invariance_determinism_and_host_path():
     est.close()
 
 
-def test_zero_linearity_bad_set_and_validation():
-    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator()
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_zero_linearity_bad_set_and_validation(kernel):
+    ce, cfg, est, r, s2, x, y, soi = _cfg2_estimator(kernel)
     x_d = torch.from_numpy(x).cuda()
     soi_d = torch.from_numpy(soi).cuda()
     z = est.estimate(torch.zeros(y.shape, dtype=torch.complex64, device="cuda"), x_d, set_of_instance=soi_d)
@@ -217,13 +233,26 @@ def test_zero_linearity_bad_set_and_validation():
     est.close()
 
 
-def test_mse_gain_on_gpu():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_mse_gain_on_gpu(kernel):
     """End-to-end sanity on config 3: GPU estimate MSE vs the true channel matches the closed form."""
     cfg = dataclasses.replace(CONFIGS[3], M=64)
     r, s2 = workload.channel_stats(cfg, 0)
     x = workload.gen_pilots(cfg, 0)
     y, H = workload.gen_instances(cfg, 0, x=x, return_channel=True)
-    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x)
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, kernel=kernel)
     mse = np.mean(np.abs(h - H) ** 2)
     cf = oracle.block_mse(r[0], s2[0], cfg.b)
     assert abs(mse / cf - 1) < 0.05
+
+
+def test_kernels_agree_and_auto():
+    """K2 (FP32 SIMT) and K3 (3xTF32 tcgen05) agree far inside the oracle tolerance."""
+    cfg = CONFIGS[3]
+    r, s2, x, y, soi = _inputs(cfg)
+    h1 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=1)
+    h2 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=2)
+    h0 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=0)
+    d = oracle.rel_fro_error_per_instance(h2, h1.astype(np.complex128))
+    assert d.max() < 2e-5
+    assert np.array_equal(h0.view(np.float32), h2.view(np.float32))   # AUTO picks K3 when it fits
