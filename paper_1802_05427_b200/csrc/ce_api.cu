@@ -53,7 +53,11 @@ struct ce_handle {
   float2 *d_Wt = nullptr;       // [n_sets][b][b] transposed
   float *d_bank = nullptr;      // K3 filter bank: hi plane then lo plane, [n_sets][nkc][NR][32] each
   size_t bank_plane = 0;        // floats per plane
-  bool tf32_ok = false;         // every window fits the K3 tile (N <= 256)
+  bool tf32_ok = false;         // every window fits the tensor-core tile (N <= 256)
+  uint16_t *d_bank16 = nullptr; // K4 filter bank: bf16 hi plane then lo plane
+  size_t bank16_plane = 0;      // elements per plane
+  int32_t last_kernel = -1;     // kernel launched by the most recent ce_estimate
+  bool even_starts = true;      // all window starts even (K4 TMA alignment)
   int32_t *d_flag = nullptr;    // [1] build error flag
   int32_t *h_flag = nullptr;    // pinned mirror
   // host-buffer path (grown on demand)
@@ -104,6 +108,7 @@ void release(ce_handle *h) {
   cudaFree(h->d_W);
   cudaFree(h->d_Wt);
   cudaFree(h->d_bank);
+  cudaFree(h->d_bank16);
   cudaFree(h->d_flag);
   cudaFreeHost(h->h_flag);
   cudaFree(h->d_stage);
@@ -133,7 +138,7 @@ int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
 
 extern "C" {
 
-const char *ce_version(void) { return "libce 0.2 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3)"; }
+const char *ce_version(void) { return "libce 0.3 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3, K4 tcgen05 bf16x3 + TMA)"; }
 
 const char *ce_status_string(int status) {
   switch (status) {
@@ -204,7 +209,10 @@ int ce_init(const ce_params *p, ce_handle **out) {
   h->n_sets = S;
   h->geo = geo;
   h->n_win = int32_t(geo.size());
-  for (auto &g : geo) h->max_kept = std::max(h->max_kept, g.o_next - g.o);
+  for (auto &g : geo) {
+    h->max_kept = std::max(h->max_kept, g.o_next - g.o);
+    if ((g.a & 1) || (N & 1)) h->even_starts = false;   // 16-byte TMA box starts and row pitch
+  }
 
   std::vector<double2> r_b(size_t(S) * b);
   for (int32_t s = 0; s < S; ++s)
@@ -216,6 +224,8 @@ int ce_init(const ce_params *p, ce_handle **out) {
     int32_t nkc, NR;
     ce::tf32x3_bank_shape(b, &nkc, &NR);
     h->bank_plane = size_t(S) * nkc * NR * 32;
+    ce::bf16x3_bank_shape(b, &nkc, &NR);
+    h->bank16_plane = size_t(S) * nkc * NR * 32;
   }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
@@ -226,6 +236,7 @@ int ce_init(const ce_params *p, ce_handle **out) {
   chk(cudaMalloc(&h->d_W, size_t(S) * b * b * sizeof(float2)));
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank, 2 * h->bank_plane * sizeof(float)));
+  if (h->tf32_ok) chk(cudaMalloc(&h->d_bank16, 2 * h->bank16_plane * sizeof(uint16_t)));
   chk(cudaMalloc(&h->d_flag, sizeof(int32_t)));
   chk(cudaMallocHost(&h->h_flag, sizeof(int32_t)));
   if (e == cudaSuccess) {
@@ -255,18 +266,25 @@ int ce_free(ce_handle *h) {
 
 int ce_set_kernel(ce_handle *h, int32_t kernel) {
   if (h == nullptr) return fail(CE_EINVAL, "ce_set_kernel: NULL handle");
-  if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT && kernel != CE_KERNEL_TF32X3)
+  if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT && kernel != CE_KERNEL_TF32X3 &&
+      kernel != CE_KERNEL_BF16X3)
     return fail(CE_EINVAL, "ce_set_kernel: unknown kernel");
-  if (kernel == CE_KERNEL_TF32X3 && !h->tf32_ok)
-    return fail(CE_EINVAL, "ce_set_kernel: TF32X3 needs 2*kept + row alignment <= 256 for every window");
+  if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3) && !h->tf32_ok)
+    return fail(CE_EINVAL, "ce_set_kernel: tensor-core kernels need 2*kept + row alignment <= 256 for every window");
+  if (kernel == CE_KERNEL_BF16X3 && !h->even_starts)
+    return fail(CE_EINVAL, "ce_set_kernel: BF16X3 needs every window start a_w even (16-byte TMA boxes)");
   h->kernel = kernel;
   return CE_OK;
 }
 
 int ce_selected_kernel(const ce_handle *h, int32_t *out) {
   if (h == nullptr || out == nullptr) return fail(CE_EINVAL, "ce_selected_kernel: NULL argument");
-  *out = (h->kernel == CE_KERNEL_TF32X3 || (h->kernel == CE_KERNEL_AUTO && h->tf32_ok)) ? CE_KERNEL_TF32X3
-                                                                                        : CE_KERNEL_SIMT;
+  if (h->last_kernel >= 0)
+    *out = h->last_kernel;
+  else if (h->kernel == CE_KERNEL_AUTO)
+    *out = !h->tf32_ok ? CE_KERNEL_SIMT : (h->even_starts ? CE_KERNEL_BF16X3 : CE_KERNEL_TF32X3);
+  else
+    *out = h->kernel;
   return CE_OK;
 }
 
@@ -286,9 +304,13 @@ int ce_build_filters(ce_handle *h, void *stream) {
   CE_CUDA(ce::launch_filter_build(h->d_r, h->d_sigma2, h->N, h->b, h->n_sets, h->d_ws, h->d_W, h->d_Wt,
                                   h->d_flag, st, &h->launches),
           "ce_build_filters: launch");
-  if (h->tf32_ok)
+  if (h->tf32_ok) {
     CE_CUDA(ce::launch_build_bank(h->d_W, h->b, h->n_sets, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches),
             "ce_build_filters: bank launch");
+    CE_CUDA(ce::launch_build_bank_bf16(h->d_W, h->b, h->n_sets, h->d_bank16, h->d_bank16 + h->bank16_plane, st,
+                                       &h->launches),
+            "ce_build_filters: bf16 bank launch");
+  }
   CE_CUDA(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st),
           "ce_build_filters: flag copy");
   CE_CUDA(cudaStreamSynchronize(st), "ce_build_filters: synchronize");
@@ -324,10 +346,21 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
   a.n_win = h->n_win;
   a.n_sets = h->n_sets;
   a.max_kept = h->max_kept;
-  const bool use_tc = h->kernel == CE_KERNEL_TF32X3 || (h->kernel == CE_KERNEL_AUTO && h->tf32_ok);
-  cudaError_t e = use_tc ? ce::launch_contract_tf32x3(a, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches)
-                         : ce::launch_contract_simt(a, st, &h->launches);
+  a.even_starts = h->even_starts;
+  int32_t k = h->kernel;
+  if (k == CE_KERNEL_AUTO)
+    k = !h->tf32_ok ? CE_KERNEL_SIMT : (ce::bf16x3_launchable(a) ? CE_KERNEL_BF16X3 : CE_KERNEL_TF32X3);
+  if (k == CE_KERNEL_BF16X3 && !ce::bf16x3_launchable(a))
+    return fail(CE_EINVAL, "ce_estimate: BF16X3 needs K <= 32, even N, even window starts, 16-byte aligned y/x");
+  cudaError_t e;
+  if (k == CE_KERNEL_BF16X3)
+    e = ce::launch_contract_bf16x3(a, h->d_bank16, h->d_bank16 + h->bank16_plane, st, &h->launches);
+  else if (k == CE_KERNEL_TF32X3)
+    e = ce::launch_contract_tf32x3(a, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches);
+  else
+    e = ce::launch_contract_simt(a, st, &h->launches);
   if (e != cudaSuccess) return cuda_fail(e, "ce_estimate: kernel launch");
+  h->last_kernel = k;
   return CE_OK;
 }
 

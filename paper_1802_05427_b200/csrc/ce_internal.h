@@ -30,6 +30,7 @@ struct ContractArgs {
   const Window *geo;       // [n_win] (device)
   const int32_t *soi;      // [T] device or nullptr
   int32_t T, M, K, N, b, n_win, n_sets, max_kept;
+  bool even_starts;        // every window start a_w is even (16-byte aligned TMA boxes, K4)
 };
 
 // K1: filter build.  Returns cudaError_t of the launches.
@@ -47,6 +48,14 @@ void tf32x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR);
 cudaError_t launch_build_bank(const float2 *d_W, int32_t b, int32_t n_sets, float *bank_hi, float *bank_lo,
                               cudaStream_t stream, int64_t *launches);
 cudaError_t launch_contract_tf32x3(const ContractArgs &a, const float *bank_hi, const float *bank_lo,
+                                   cudaStream_t stream, int64_t *launches);
+
+// K4: tcgen05 BF16x3 contraction with TMA-fed raw ring (same bank geometry as K3, bf16 planes).
+void bf16x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR);
+bool bf16x3_launchable(const ContractArgs &a);
+cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets, uint16_t *bank_hi,
+                                   uint16_t *bank_lo, cudaStream_t stream, int64_t *launches);
+cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches);
 
 void set_last_error(const std::string &msg);
