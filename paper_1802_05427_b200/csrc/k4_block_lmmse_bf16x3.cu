@@ -9,16 +9,17 @@
 // B_r^T rows 2i / 2i+1 = (Re W_ij, -Im W_ij) / (Im W_ij, Re W_ij)).  BF16 runs the tensor core at
 // twice the TF32 rate and halves the operand bytes in shared memory and L2.
 //
-// Pipeline (persistent CTAs, one per SM, 352 threads):
-//   warp 8    : raw producer -- 2D TMA (cp.async.bulk.tensor) of the raw y box [128 rows x 16
+// Pipeline (persistent CTAs, one per SM, 480 threads):
+//   warp 12   : raw producer -- 2D TMA (cp.async.bulk.tensor) of the raw y box [128 rows x 16
 //               complex] and the pilot box [K rows x 16 complex] of each K chunk into a 3-deep
 //               raw ring (no registers held, ~48 KB of HBM reads in flight per SM)
-//   warps 0-3 : transform -- raw ring -> LS = y conj(x)/|x|^2 -> bf16 hi/lo -> SWIZZLE_64B K-major
-//               A tiles of the 3-deep AB ring; fence.proxy.async; arrive a_full
-//   warp 10   : B producer -- cp.async.bulk of the bf16 hi/lo bank chunk (pre-swizzled SW64 image)
-//   warp 9    : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> ab_empty;
+//   warps 0-7 : transform -- per chunk: LS factors f = conj(x)/|x|^2 computed once per (k, j) in
+//               place in the raw pilot slot (named barrier), then LS = y f -> bf16 hi/lo ->
+//               SWIZZLE_64B K-major A tiles of the 3-deep AB ring; fence.proxy.async; arrive a_full
+//   warp 14   : B producer -- cp.async.bulk of the bf16 hi/lo bank chunk (pre-swizzled SW64 image)
+//   warp 13   : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> ab_empty;
 //               per tile commit -> tmem_full[acc] (two 256-column accumulators)
-//   warps 4-7 : epilogue -- tcgen05.ld 32 columns, transpose through smem, coalesced stores
+//   warps 8-11: epilogue -- tcgen05.ld 32 columns, transpose through smem, coalesced stores
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -29,7 +30,8 @@
 namespace ce {
 namespace {
 
-constexpr int K4_THREADS = 352;
+constexpr int K4_THREADS = 480;            // 15 warps: 8 transform, 4 epilogue, 3 single-thread roles
+constexpr int NTR = 256;                   // transform threads
 constexpr int CK = 16;                     // complex per K chunk = 32 bf16 = 64-byte rows
 constexpr int S_AB = 3;                    // A/B stages
 constexpr int S_RAW = 3;                   // raw y/x stages
@@ -89,6 +91,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_addr, float hi_addr) {
 }
 __device__ __forceinline__ float bf16_lo_f(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi_f(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx, K4Params p) {
@@ -113,10 +120,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < S_RAW; ++s) {
       mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], 128);
+      mbar_init(&raw_empty[s], NTR);
     }
     for (int s = 0; s < S_AB; ++s) {
-      mbar_init(&a_full[s], 128);
+      mbar_init(&a_full[s], NTR);
       mbar_init(&b_full[s], 1);
       mbar_init(&ab_empty[s], 1);
     }
@@ -126,18 +133,18 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == 13) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int nks_total = (2 * p.b + 15) / 16;   // 16-element (bf16) MMA K steps over 2b
 
-  if (warp == 8) {
+  if (warp == 12) {
     // ---------------------------------------------------------------- raw producer (TMA)
     if (lane == 0) {
       const uint32_t xbytes = uint32_t(p.K) * CK * 8;
@@ -155,38 +162,44 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 8) {
     // ---------------------------------------------------------------- transform
     const int jp = tid & 7;            // complex pair 2jp, 2jp+1 of the 16-complex chunk
-    const int rb = tid >> 3;           // rows rb + 16 i, i < 8
+    const int rb = tid >> 3;           // rows rb + 32 i, i < 4
     int it = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       const Tile4 ti = decode4(p, tile);
       const int c_first = ti.ct * TM + rb;
       const int x_first = c_first % p.K;
-      const int x_step = 16 % p.K;
+      const int x_step = 32 % p.K;
       for (int kc = 0; kc < p.nkc; ++kc, ++it) {
         const int sr = it % S_RAW, sa = it % S_AB;
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
-        mbar_wait(&ab_empty[sa], ((it / S_AB) & 1) ^ 1);
         const float4 *ry = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE);
-        const float4 *rx = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE + RAWY);
+        float4 *rx = reinterpret_cast<float4 *>(raw + sr * RAW_STAGE + RAWY);
+        // LS factors in place: f = conj(x) / |x|^2 for the K x 16 pilots of this chunk
+        const int j0 = kc * CK + 2 * jp;                // window-relative complex index
+        if (tid < p.K * 8) {
+          const float4 xv = rx[tid];
+          const float i0 = rcp_approx(xv.x * xv.x + xv.y * xv.y);
+          const float i1 = rcp_approx(xv.z * xv.z + xv.w * xv.w);
+          const bool ok0 = kc * CK + 2 * (tid & 7) < p.b, ok1 = kc * CK + 2 * (tid & 7) + 1 < p.b;
+          rx[tid] = make_float4(ok0 ? xv.x * i0 : 0.f, ok0 ? -xv.y * i0 : 0.f, ok1 ? xv.z * i1 : 0.f,
+                                ok1 ? -xv.w * i1 : 0.f);   // zero factor masks the K tail (j >= b)
+        }
+        named_bar_sync(1, NTR);
+        mbar_wait(&ab_empty[sa], ((it / S_AB) & 1) ^ 1);
         uint8_t *ah = ab + sa * AB_STAGE;
         uint8_t *al = ah + A_PLANE;
-        const int j0 = kc * CK + 2 * jp;                // window-relative complex index
-        const bool ok0 = j0 < p.b, ok1 = j0 + 1 < p.b;
+        (void)j0;
         int xr = x_first;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = rb + 16 * i;
+        for (int i = 0; i < 4; ++i) {
+          const int r = rb + 32 * i;
           const float4 yv = ry[r * 8 + jp];
-          const float4 xv = rx[xr * 8 + jp];
-          const float inv0 = 1.0f / (xv.x * xv.x + xv.y * xv.y);
-          const float inv1 = 1.0f / (xv.z * xv.z + xv.w * xv.w);
-          float l0r = (yv.x * xv.x + yv.y * xv.y) * inv0, l0i = (yv.y * xv.x - yv.x * xv.y) * inv0;
-          float l1r = (yv.z * xv.z + yv.w * xv.w) * inv1, l1i = (yv.w * xv.z - yv.z * xv.w) * inv1;
-          if (!ok0) l0r = l0i = 0.f;
-          if (!ok1) l1r = l1i = 0.f;
+          const float4 fv = rx[xr * 8 + jp];
+          const float l0r = yv.x * fv.x - yv.y * fv.y, l0i = yv.x * fv.y + yv.y * fv.x;
+          const float l1r = yv.z * fv.z - yv.w * fv.w, l1i = yv.z * fv.w + yv.w * fv.z;
           const uint32_t h0 = pack_bf16(l0r, l0i), h1 = pack_bf16(l1r, l1i);
           const uint32_t g0 = pack_bf16(l0r - bf16_lo_f(h0), l0i - bf16_hi_f(h0));
           const uint32_t g1 = pack_bf16(l1r - bf16_lo_f(h1), l1i - bf16_hi_f(h1));
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         mbar_arrive(&raw_empty[sr]);
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < 12) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;
     float *stage = epi + q * 32 * EPI_STRIDE;
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tmem_empty[acc]);
     }
-  } else if (warp == 10) {
+  } else if (warp == 14) {
     // ---------------------------------------------------------------- B producer
     if (lane == 0) {
       int it = 0;
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       }
     }
   } else {
-    // ---------------------------------------------------------------- MMA issuer (warp 9)
+    // ---------------------------------------------------------------- MMA issuer (warp 13)
     if (lane == 0) {
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
@@ -297,7 +310,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
