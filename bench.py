@@ -193,6 +193,7 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     import paper_1802_05427_b200 as ce
+    from paper_1802_05427_b200.shard import antenna_shard
 
     world, rank, local = _dist_env()
     if not torch.cuda.is_available():
@@ -205,8 +206,10 @@ def run_ours(args, cfg):
     r, s2 = workload.channel_stats(cfg, 0)
     soi = workload.set_of_instance(cfg)
     x = workload.gen_pilots(cfg, 0)
-    # rank r estimates antennas of its own shard of the global batch: seeded by rank
-    y = workload.gen_instances(cfg, 0 + rank, x=x)
+    # weak scaling: the global batch has world*M antennas; rank r owns the contiguous block
+    # [r*M, (r+1)*M) (shard.antenna_shard), drawn with the per-(t, m) seeds of the full draw
+    m_lo, m_hi = antenna_shard(world * cfg.M, world, rank)
+    y = workload.gen_instances(cfg, 0, m_lo=m_lo, m_hi=m_hi, x=x)
     est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2, kernel=args.kernel)
     stream = torch.cuda.current_stream()
     tb0 = time.perf_counter()
