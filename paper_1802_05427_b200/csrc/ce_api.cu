@@ -337,6 +337,7 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
   a.h = out;
   a.Wt = h->d_Wt;
   a.geo = h->d_geo;
+  a.geo_host = h->geo.data();
   a.soi = soi;
   a.T = T;
   a.M = M;

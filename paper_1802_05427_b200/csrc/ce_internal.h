@@ -28,6 +28,7 @@ struct ContractArgs {
   float2 *h;               // [T][M][K][N]
   const float2 *Wt;        // [n_sets][b][b] transposed filters: Wt[s][j][i] = W[s][i][j]
   const Window *geo;       // [n_win] (device)
+  const Window *geo_host;  // [n_win] (host copy; K4 passes small tables in its kernel parameters)
   const int32_t *soi;      // [T] device or nullptr
   int32_t T, M, K, N, b, n_win, n_sets, max_kept;
   bool even_starts;        // every window start a_w is even (16-byte aligned TMA boxes, K4)

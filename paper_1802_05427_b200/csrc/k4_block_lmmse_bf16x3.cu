@@ -1,28 +1,39 @@
 // K4 -- fused LS + block-LMMSE contraction on tcgen05 (kind::f16, BF16 operands), error-compensated
 // "BF16x3":  D = A_hi B_hi + A_hi B_lo + A_lo B_hi,  X_hi = bf16_rn(X), X_lo = bf16_rn(X - X_hi),
 // FP32 accumulation in TMEM.  Per-product error <= ~3 * 2^-18 (the dropped A_lo B_lo term and the
-// rounding of the lo parts); DESIGN.md §5 derives the bound and the emulation that measured
-// 1.4e-6 relative Frobenius error on configs 2-5 against the 1e-4 bar.
+// rounding of the lo parts); reading B1 derives the bound (measured ~1e-6 relative Frobenius
+// error on configs 2-5 against the 1e-4 bar).
 //
 // Same operation as K2/K3 (Eq. 12 per block, LS of Eq. 9 fused into the load) and
 // the same complex -> real embedding as K3 (A = interleaved LS row, D = interleaved output row,
-// B_r^T rows 2i / 2i+1 = (Re W_ij, -Im W_ij) / (Im W_ij, Re W_ij)).  BF16 runs the tensor core at
-// twice the TF32 rate and halves the operand bytes in shared memory and L2.
+// B_r^T rows 2i / 2i+1 = (Re W_ij, -Im W_ij) / (Im W_ij, Re W_ij)).
 //
-// Pipeline (persistent CTAs, one per SM, 480 threads):
-//   warp 12   : raw producer -- 2D TMA (cp.async.bulk.tensor) of the raw y box [128 rows x 16
-//               complex] and the pilot box [K rows x 16 complex] of each K chunk into a 3-deep
-//               raw ring (no registers held, ~48 KB of HBM reads in flight per SM)
-//   warps 0-7 : transform -- per chunk: LS factors f = conj(x)/|x|^2 computed once per (k, j) in
-//               place in the raw pilot slot (named barrier), then LS = y f -> bf16 hi/lo ->
-//               SWIZZLE_64B K-major A tiles of the 3-deep AB ring; fence.proxy.async; arrive a_full
-//   warp 14   : B producer -- cp.async.bulk of the bf16 hi/lo bank chunk (pre-swizzled SW64 image)
-//   warp 13   : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> ab_empty;
+// Work unit: a tile = (instance t, window w, 128-column block ct).  CG = 1: one CTA per tile, M = 128.
+// CG = 2 (CE_K4_CG=2, experimental): a CTA pair runs cta_group::2 MMAs with M = 256 over two column
+// blocks; each CTA stages only half of the filter operand.  Measured slower than CG = 1 on configs 3
+// and 5 (the per-chunk peer -> leader handshake lengthens every stage's turnaround), so CG = 1 is the
+// default.
+//
+// Pipeline (persistent, one CTA per SM, 480 threads):
+//   warp 12   : raw producer -- 2D TMA of the raw y box [128 rows x 16 complex] and the pilot box
+//               [K rows x 16 complex] of each K chunk into a 3-deep raw ring
+//   warps 0-7 : transform -- LS factors f = conj(x)/|x|^2 once per (k, j) in place in the raw pilot
+//               slot (named barrier), then LS = y f -> bf16 hi/lo -> SWIZZLE_64B K-major A tiles of the
+//               3-deep A/B ring; fence.proxy.async; arrive a_full
+//   warp 14   : B producer -- cp.async.bulk of this CTA's rows of the bf16 hi/lo bank chunk
+//               (pre-swizzled SW64 image)
+//   warp 13   : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> st_empty;
 //               per tile commit -> tmem_full[acc] (two 256-column accumulators)
-//   warps 8-11: epilogue -- tcgen05.ld 32 columns, transpose through smem, coalesced stores
+//   warps 8-11: epilogue -- tcgen05.ld 16x256b (4 threads hold 4 consecutive outputs of a row), direct
+//               8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes
+// The window table rides in the kernel parameters (no dependent global load before the first TMA), and
+// the kernel is launched with programmatic stream serialization (PDL): its launch overlaps the previous
+// kernel's tail; griddepcontrol.wait precedes every global access.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cstdlib>
 
 #include "ce_internal.h"
 #include "tc_ptx.cuh"
@@ -30,57 +41,83 @@
 namespace ce {
 namespace {
 
+// Optional per-CTA event trace (tools/k4_trace.cu builds with -DCE_K4_TRACE; the product build has none).
+#ifdef CE_K4_TRACE
+__device__ unsigned long long *g_k4_trace;
+#define K4TR(slot)                                                             \
+  do {                                                                         \
+    if (g_k4_trace) g_k4_trace[size_t(blockIdx.x) * 256 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define K4TR(slot) \
+  do {             \
+  } while (0)
+#endif
+
 constexpr int K4_THREADS = 480;            // 15 warps: 8 transform, 4 epilogue, 3 single-thread roles
 constexpr int NTR = 256;                   // transform threads
 constexpr int CK = 16;                     // complex per K chunk = 32 bf16 = 64-byte rows
-constexpr int S_AB = 3;                    // A/B stages
-constexpr int S_RAW = 3;                   // raw y/x stages
-constexpr int TM = 128;                    // MMA M (columns c per tile)
+constexpr int TM = 128;                    // A rows (columns c) per CTA
 constexpr int NMAXW = 256;                 // MMA N max (2*kept + row alignment)
 constexpr int KMAX = 32;                   // pilot rows per raw stage (K <= 32)
+constexpr int S_RAW = 3;                   // raw y/x stages
 constexpr int A_PLANE = TM * 64;           // 8 KB
-constexpr int B_PLANE = NMAXW * 64;        // 16 KB
-constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;      // 48 KB
 constexpr int RAWY = TM * CK * 8;          // 16 KB
 constexpr int RAWX = KMAX * CK * 8;        // 4 KB
 constexpr int RAW_STAGE = RAWY + RAWX;     // 20 KB
-constexpr int EPI_STRIDE = 34;
-constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;
+constexpr int EPI_BYTES = 0;               // epilogue stores straight from TMEM registers
 constexpr int BAR_BYTES = 256;
-constexpr int K4_SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
+
+// CG = CTAs per MMA: 1 (cta_group::1, M = 128) or 2 (CTA pair, cta_group::2, M = 256: each CTA stages its
+// own 128 A rows and HALF of the filter operand's N rows, so per-SM filter traffic and tensor-core smem
+// reads of B halve).
+template <int CG>
+struct K4Cfg {
+  static constexpr int S_AB = CG == 1 ? 3 : 4;                   // A/B stages
+  static constexpr int B_PLANE = (NMAXW / CG) * 64;              // 16 KB / 8 KB
+  static constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;     // 48 KB / 32 KB
+  static constexpr int SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+};
 
 struct K4Params {
   float2 *h;
   const uint16_t *bank_hi;   // bf16 [n_sets][nkc][NR][32] swizzled SW64 rows
   const uint16_t *bank_lo;
-  const Window *geo;
+  const Window *geo;         // device window table (read only when n_win > MAXW_PARAM)
   const int32_t *soi;
-  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct, n_tiles;
+  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
+  int n_ctg;                 // column-block groups per (t, w): ceil(n_ct / CG)
+  int n_groups;              // T * n_win * n_ctg
+  Window geo_s[MAXW_PARAM];
 };
 
 struct Tile4 {
-  int t, ct, a, o, kept, n0, off, nw, set;
-  bool set_ok;
+  int t, ct, a, o, kept, n0, off, nw;
 };
 
-__device__ __forceinline__ Tile4 decode4(const K4Params &p, int tile) {
+__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank, int CG) {
   Tile4 ti;
-  ti.ct = tile % p.n_ct;
-  const int rest = tile / p.n_ct;
+  const int ctg = g % p.n_ctg;
+  const int rest = g / p.n_ctg;
   const int w = rest % p.n_win;
   ti.t = rest / p.n_win;
-  const Window g = p.geo[w];
-  ti.a = g.a;
-  ti.o = g.o;
-  ti.kept = g.o_next - g.o;
-  const int row2 = 2 * (g.o - g.a);
+  ti.ct = ctg * CG + rank;
+  const Window gw = p.n_win <= MAXW_PARAM ? p.geo_s[w] : p.geo[w];
+  ti.a = gw.a;
+  ti.o = gw.o;
+  ti.kept = gw.o_next - gw.o;
+  const int row2 = 2 * (gw.o - gw.a);
   ti.n0 = row2 & ~7;
   ti.off = row2 - ti.n0;
   ti.nw = (ti.off + 2 * ti.kept + 15) & ~15;
-  const int s = p.soi ? p.soi[ti.t] : 0;
-  ti.set_ok = s >= 0 && s < p.n_sets;
-  ti.set = ti.set_ok ? s : 0;
   return ti;
+}
+
+// statistic set of instance t, or -1 when set_of_instance[t] is out of range (outputs become NaN)
+__device__ __forceinline__ int tile_set(const K4Params &p, int t) {
+  const int s = p.soi ? p.soi[t] : 0;
+  return (s >= 0 && s < p.n_sets) ? s : -1;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo_addr, float hi_addr) {
@@ -97,11 +134,18 @@ __device__ __forceinline__ float rcp_approx(float v) {
   return r;
 }
 
+template <int CG>
 __global__ void __launch_bounds__(K4_THREADS, 1)
-    k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx, K4Params p) {
+    k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
+              const __grid_constant__ K4Params p) {
+  using Cfg = K4Cfg<CG>;
+  constexpr int S_AB = Cfg::S_AB;
+  constexpr int B_PLANE = Cfg::B_PLANE;
+  constexpr int AB_STAGE = Cfg::AB_STAGE;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
-  // visible to the compiler: LDS/STS instead of generic LD/ST)
+  // visible to the compiler: LDS/STS instead of generic LD/ST); the same offsets in both CTAs of a pair,
+  // which the pair MMA (peer operands at the same smem offset) and the multicast commits rely on
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
   uint8_t *raw = smem + S_AB * AB_STAGE;                // [S_RAW][y 16 KB | x 4 KB]
@@ -109,15 +153,26 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(epi) + EPI_BYTES);
   uint64_t *raw_full = bars;                            // [S_RAW]
   uint64_t *raw_empty = bars + S_RAW;                   // [S_RAW]
-  uint64_t *a_full = bars + 2 * S_RAW;                  // [S_AB]
-  uint64_t *b_full = a_full + S_AB;                     // [S_AB]
-  uint64_t *ab_empty = b_full + S_AB;                   // [S_AB]
-  uint64_t *tmem_full = ab_empty + S_AB;                // [2]
-  uint64_t *tmem_empty = tmem_full + 2;                 // [2]
+  uint64_t *a_full = bars + 2 * S_RAW;                  // [S_AB]  local transform done
+  uint64_t *b_full = a_full + S_AB;                     // [S_AB]  local filter slice landed
+  uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
+  uint64_t *peer_ready = st_empty + S_AB;               // [S_AB]  (pair leader) peer's stage is full
+  uint64_t *tmem_full = peer_ready + S_AB;              // [2]
+  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp (x CG)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = CG > 1 ? int(cluster_ctarank()) : 0;
+  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;
+#ifdef CE_K4_TRACE
+  if (tid == 0 && g_k4_trace) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_k4_trace[size_t(blockIdx.x) * 256 + 0] = gt;
+  }
+#endif
   if (tid == 0) {
+    K4TR(1);
     for (int s = 0; s < S_RAW; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], NTR);
@@ -125,11 +180,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     for (int s = 0; s < S_AB; ++s) {
       mbar_init(&a_full[s], NTR);
       mbar_init(&b_full[s], 1);
-      mbar_init(&ab_empty[s], 1);
+      mbar_init(&st_empty[s], 1);
+      mbar_init(&peer_ready[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 128);
+      mbar_init(&tmem_empty[i], 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -137,11 +193,22 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
   }
-  if (warp == 13) tmem_alloc(tmem_slot, 512);
+  if (warp == 13) {
+    if (CG == 1)
+      tmem_alloc(tmem_slot, 512);
+    else
+      tmem_alloc2(tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG > 1) cluster_sync();         // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (tid == 0) {
+    pdl_launch_dependents();          // the next kernel in the stream may launch (it waits for our exit)
+    K4TR(2);
+  }
+  pdl_wait();                         // the previous kernel's writes are visible from here on
   const int nks_total = (2 * p.b + 15) / 16;   // 16-element (bf16) MMA K steps over 2b
 
   if (warp == 12) {
@@ -149,13 +216,14 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     if (lane == 0) {
       const uint32_t xbytes = uint32_t(p.K) * CK * 8;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        const Tile4 ti = decode4(p, tile);
+      for (int g = unit; g < p.n_groups; g += n_units) {
+        const Tile4 ti = decode4(p, g, rank, CG);
         const int row0 = ti.t * p.cols + ti.ct * TM;
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_RAW;
           mbar_wait(&raw_empty[s], ((it / S_RAW) & 1) ^ 1);
           mbar_arrive_expect_tx(&raw_full[s], RAWY + xbytes);
+          if (it < 24) K4TR(8 + it);
           const int f0 = 2 * (ti.a + kc * CK);        // first float of the chunk in the row
           tma_load_2d(raw + s * RAW_STAGE, &tmy, f0, row0, &raw_full[s]);
           tma_load_2d(raw + s * RAW_STAGE + RAWY, &tmx, f0, ti.t * p.K, &raw_full[s]);
@@ -167,18 +235,18 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int jp = tid & 7;            // complex pair 2jp, 2jp+1 of the 16-complex chunk
     const int rb = tid >> 3;           // rows rb + 32 i, i < 4
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-      const Tile4 ti = decode4(p, tile);
+    for (int g = unit; g < p.n_groups; g += n_units) {
+      const Tile4 ti = decode4(p, g, rank, CG);
       const int c_first = ti.ct * TM + rb;
       const int x_first = c_first % p.K;
       const int x_step = 32 % p.K;
       for (int kc = 0; kc < p.nkc; ++kc, ++it) {
         const int sr = it % S_RAW, sa = it % S_AB;
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
+        if (tid == 0 && it < 24) K4TR(32 + it);
         const float4 *ry = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE);
         float4 *rx = reinterpret_cast<float4 *>(raw + sr * RAW_STAGE + RAWY);
         // LS factors in place: f = conj(x) / |x|^2 for the K x 16 pilots of this chunk
-        const int j0 = kc * CK + 2 * jp;                // window-relative complex index
         if (tid < p.K * 8) {
           const float4 xv = rx[tid];
           const float i0 = rcp_approx(xv.x * xv.x + xv.y * xv.y);
@@ -188,10 +256,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
                                 ok1 ? -xv.w * i1 : 0.f);   // zero factor masks the K tail (j >= b)
         }
         named_bar_sync(1, NTR);
-        mbar_wait(&ab_empty[sa], ((it / S_AB) & 1) ^ 1);
+        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
         uint8_t *ah = ab + sa * AB_STAGE;
         uint8_t *al = ah + A_PLANE;
-        (void)j0;
         int xr = x_first;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -211,77 +278,112 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           if (xr >= p.K) xr -= p.K;
         }
         fence_proxy_async();
+        if (tid == 0 && it < 24) K4TR(56 + it);
         mbar_arrive(&a_full[sa]);
         mbar_arrive(&raw_empty[sr]);
       }
     }
   } else if (warp < 12) {
     // ---------------------------------------------------------------- epilogue
+    // TMEM -> registers (16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row)
+    // -> direct 8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes.
     const int q = warp & 3;
-    float *stage = epi + q * 32 * EPI_STRIDE;
+    const int rA = lane >> 2, cq = lane & 3;
     int lt = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
-      const Tile4 ti = decode4(p, tile);
+    for (int g = unit; g < p.n_groups; g += n_units, ++lt) {
+      const Tile4 ti = decode4(p, g, rank, CG);
+      const bool set_ok = tile_set(p, ti.t) >= 0;
       const int acc = lt & 1;
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
       tc_fence_after();
+      if (tid == 256 && lt < 8) K4TR(136 + lt);
       const int nf = 2 * ti.kept;
       const int ncb = (ti.off + nf + 31) / 32;
-      const int row_base = ti.ct * TM + q * 32;
+      const int c0 = ti.ct * TM + q * 32 + rA;         // rows c0, c0 + 8, c0 + 16, c0 + 24
+      float2 *hrow = p.h + (size_t(ti.t) * p.cols + c0) * p.N + ti.o;
+      const size_t row8 = size_t(8) * p.N;
       const float qnan = __int_as_float(0x7fc00000);
       for (int cb = 0; cb < ncb; ++cb) {
-        float v[32];
-        tmem_ld32(tmem_base + uint32_t(acc * NMAXW + cb * 32) + (uint32_t(q * 32) << 16), v);
+        uint32_t v0[16], v1[16];
+        const uint32_t ta = tmem_base + uint32_t(acc * NMAXW + cb * 32) + (uint32_t(q * 32) << 16);
+        tmem_ld16x256b_x4(ta, v0);                       // lanes q*32 + 0..15
+        tmem_ld16x256b_x4(ta + (16u << 16), v1);         // lanes q*32 + 16..31
+        tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 32; u += 2)
-          *reinterpret_cast<float2 *>(stage + lane * EPI_STRIDE + u) = make_float2(v[u], v[u + 1]);
-        __syncwarp();
-        const int f = cb * 32 - ti.off + 2 * (lane & 15);
-        const bool fok = f >= 0 && f < nf;
-#pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 2) {
-          const int r = rr + (lane >> 4);
-          const int c = row_base + r;
-          if (fok && c < p.cols) {
-            float2 val = *reinterpret_cast<const float2 *>(stage + r * EPI_STRIDE + 2 * (lane & 15));
-            if (!ti.set_ok) val = make_float2(qnan, qnan);
-            p.h[(size_t(ti.t) * p.cols + c) * p.N + ti.o + (f >> 1)] = val;
+        for (int m = 0; m < 4; ++m) {
+          const int f = cb * 32 + 8 * m + 2 * cq - ti.off;   // output float index within the kept range
+          if (f >= 0 && f < nf) {
+            const int ci = f >> 1;
+            float2 a0 = make_float2(__uint_as_float(v0[4 * m]), __uint_as_float(v0[4 * m + 1]));
+            float2 a1 = make_float2(__uint_as_float(v0[4 * m + 2]), __uint_as_float(v0[4 * m + 3]));
+            float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
+            float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
+            if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
+            if (c0 < p.cols) hrow[ci] = a0;
+            if (c0 + 8 < p.cols) hrow[row8 + ci] = a1;
+            if (c0 + 16 < p.cols) hrow[2 * row8 + ci] = a2;
+            if (c0 + 24 < p.cols) hrow[3 * row8 + ci] = a3;
           }
         }
-        __syncwarp();
       }
-      tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
+      if (tid == 256 && lt < 8) K4TR(144 + lt);
+      if (lane == 0) {
+        tc_fence_before();
+        if (CG == 1 || rank == 0)
+          mbar_arrive(&tmem_empty[acc]);
+        else
+          mbar_arrive_remote(&tmem_empty[acc], 0);      // the pair leader's MMA waits on both CTAs
+      }
     }
   } else if (warp == 14) {
-    // ---------------------------------------------------------------- B producer
+    // ---------------------------------------------------------------- B producer (this CTA's N rows)
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        const Tile4 ti = decode4(p, tile);
-        const uint32_t bytes = uint32_t(ti.nw) * 64;
+      for (int g = unit; g < p.n_groups; g += n_units) {
+        const Tile4 ti = decode4(p, g, rank, CG);
+        const int set = max(tile_set(p, ti.t), 0);
+        const int rows = ti.nw / CG;                           // multiple of 8 (nw is a multiple of 16)
+        const uint32_t bytes = uint32_t(rows) * 64;            // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
-          mbar_wait(&ab_empty[s], ((it / S_AB) & 1) ^ 1);
+          mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
-          const size_t src = ((size_t(ti.set) * p.nkc + kc) * p.NR + ti.n0) * 32;   // bf16 elements
+          if (it < 24) K4TR(80 + it);
+          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * rows) * 32;   // bf16 elements
           uint8_t *bh = ab + s * AB_STAGE + 2 * A_PLANE;
           bulk_g2s(bh, p.bank_hi + src, bytes, &b_full[s]);
           bulk_g2s(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s]);
         }
       }
+      // drain: the commits of the last use of every stage have arrived here, so nothing arrives on this
+      // CTA's barriers after the closing barrier
+      for (int i = 0; i < S_AB; ++i, ++it) mbar_wait(&st_empty[it % S_AB], ((it / S_AB) & 1) ^ 1);
     }
   } else {
-    // ---------------------------------------------------------------- MMA issuer (warp 13)
-    if (lane == 0) {
+    // ---------------------------------------------------------------- MMA issuer / pair forwarder (warp 13)
+    if (lane == 0 && CG == 2 && rank == 1) {
+      // pair follower: tell the leader when this CTA's half of each stage is in shared memory
+      int it = 0;
+      for (int g = unit; g < p.n_groups; g += n_units)
+        for (int kc = 0; kc < p.nkc; ++kc, ++it) {
+          const int s = it % S_AB;
+          const uint32_t ph = (it / S_AB) & 1;
+          mbar_wait(&a_full[s], ph);
+          mbar_wait(&b_full[s], ph);
+          mbar_arrive_remote(&peer_ready[s], 0);
+        }
+    } else if (lane == 0) {
       int it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
-        const Tile4 ti = decode4(p, tile);
+      for (int g = unit; g < p.n_groups; g += n_units, ++lt) {
+        const Tile4 ti = decode4(p, g, rank, CG);
         const int acc = lt & 1;
-        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128
+        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128 * CG
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(ti.nw >> 3) << 17) |
-                               (uint32_t(TM >> 4) << 24);
-        mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+                               (uint32_t((TM * CG) >> 4) << 24);
+        if (CG == 1)
+          mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+        else
+          mbar_wait_cluster(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * NMAXW);
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
@@ -289,7 +391,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const uint32_t ph = (it / S_AB) & 1;
           mbar_wait(&a_full[s], ph);
           mbar_wait(&b_full[s], ph);
+          if (CG == 2) mbar_wait_cluster(&peer_ready[s], ph);
           tc_fence_after();
+          if (it < 24) K4TR(104 + it);
           uint8_t *st = ab + s * AB_STAGE;
           const uint64_t ah = sw64_desc(smem_u32(st));
           const uint64_t al = sw64_desc(smem_u32(st + A_PLANE));
@@ -298,22 +402,41 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const int nks = min(2, nks_total - 2 * kc);
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t adv = uint64_t(2 * ks);      // +32 bytes along K
-            mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-            mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
-            mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+            if (CG == 1) {
+              mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+              mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
+              mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+            } else {
+              mma_bf16_pair(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+              mma_bf16_pair(d, ah + adv, bl + adv, idesc, 1u);
+              mma_bf16_pair(d, al + adv, bh + adv, idesc, 1u);
+            }
           }
-          mma_commit(&ab_empty[s]);
+          if (CG == 1)
+            mma_commit(&st_empty[s]);
+          else
+            mma_commit_pair(&st_empty[s]);
         }
-        mma_commit(&tmem_full[acc]);
+        if (CG == 1)
+          mma_commit(&tmem_full[acc]);
+        else
+          mma_commit_pair(&tmem_full[acc]);
+        if (lt < 8) K4TR(128 + lt);
       }
     }
   }
   tc_fence_before();
+  if (tid == 256) K4TR(3);
   __syncthreads();
+  if (CG > 1) cluster_sync();
+  if (tid == 0) K4TR(4);
   if (warp == 13) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (CG == 1)
+      tmem_dealloc(tmem_base, 512);
+    else
+      tmem_dealloc2(tmem_base, 512);
   }
 }
 
@@ -374,7 +497,82 @@ bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_ro
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor maps are a pure function of (pointer, N, rows, box rows): cache the last few per host thread so
+// back-to-back calls on the same buffers skip the driver encode.
+struct MapCacheEntry {
+  const void *ptr;
+  int N, box_rows;
+  long long rows;
+  CUtensorMap map;
+};
+bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
+  constexpr int NC = 16;
+  static thread_local MapCacheEntry cache[NC];
+  static thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i)
+    if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows) {
+      *m = cache[i].map;
+      return true;
+    }
+  if (!make_map(m, ptr, N, rows, box_rows)) return false;
+  MapCacheEntry &e = cache[next];
+  e = MapCacheEntry{ptr, N, box_rows, rows, *m};
+  next = (next + 1) % NC;
+  if (used < NC) ++used;
+  return true;
+}
+
+// Per-device launch facts: smem attributes set once, SM count, and how many CTA pairs can be resident
+// at once (a pair needs two free SMs of one TPC).
+struct DevInfo {
+  bool init = false;
+  int num_sms = 0;
+  int max_pairs = 0;
+};
+cudaError_t dev_info(DevInfo **out) {
+  static DevInfo infos[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  DevInfo &d = infos[dev];
+  if (!d.init) {
+    e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k4_bf16x3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<1>::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k4_bf16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<2>::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(d.num_sms / 2 * 2));
+    cfg.blockDim = dim3(K4_THREADS);
+    cfg.dynamicSmemBytes = K4Cfg<2>::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k4_bf16x3<2>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    d.max_pairs = n;
+    d.init = true;
+  }
+  *out = &d;
+  return cudaSuccess;
+}
+
 }  // namespace
+
+#ifdef CE_K4_TRACE
+extern "C" int ce_k4_trace_set(void *dptr) {
+  return int(cudaMemcpyToSymbol(g_k4_trace, &dptr, sizeof(dptr)));
+}
+#endif
 
 void bf16x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR) {
   *nkc = (2 * b + 31) / 32;
@@ -401,6 +599,10 @@ cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets,
 cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches) {
   if (!bf16x3_launchable(a)) return cudaErrorNotSupported;
+  if (a.n_win <= MAXW_PARAM && a.geo_host == nullptr) return cudaErrorInvalidValue;
+  DevInfo *di = nullptr;
+  cudaError_t e = dev_info(&di);
+  if (e != cudaSuccess) return e;
   K4Params p;
   p.h = a.h;
   p.bank_hi = bank_hi;
@@ -416,23 +618,44 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   bf16x3_bank_shape(a.b, &p.nkc, &p.NR);
   p.cols = a.M * a.K;
   p.n_ct = (p.cols + TM - 1) / TM;
-  const long long tiles = (long long)a.T * a.n_win * p.n_ct;
-  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  p.n_tiles = int(tiles);
+  for (int w = 0; w < MAXW_PARAM; ++w) p.geo_s[w] = w < a.n_win && a.geo_host ? a.geo_host[w] : Window{0, 0, 0};
+  // CTA pairs when the column blocks pair up exactly and pairs can cover (nearly) every SM; CE_K4_CG=1|2
+  // overrides (experiments and tests)
+  const char *env = std::getenv("CE_K4_CG");
+  const int want = env ? std::atoi(env) : 0;
+  int CG = 1;   // measured: the pair's per-chunk cross-CTA handshake costs more than the halved B traffic saves
+  if (want == 1) CG = 1;
+  if (want == 2 && di->max_pairs > 0) CG = 2;
+  p.n_ctg = (p.n_ct + CG - 1) / CG;
+  const long long groups = (long long)a.T * a.n_win * p.n_ctg;
+  if (groups > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  p.n_groups = int(groups);
   CUtensorMap tmy, tmx;
-  if (!make_map(&tmy, a.y, a.N, (long long)a.T * p.cols, TM) || !make_map(&tmx, a.x, a.N, (long long)a.T * a.K, a.K))
+  if (!cached_map(&tmy, a.y, a.N, (long long)a.T * p.cols, TM) ||
+      !cached_map(&tmx, a.x, a.N, (long long)a.T * a.K, a.K))
     return cudaErrorInvalidValue;
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int max_units = CG == 1 ? di->num_sms : di->max_pairs;
+  const int n_units = int(groups < max_units ? groups : max_units);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(n_units * CG));
+  cfg.blockDim = dim3(K4_THREADS);
+  cfg.dynamicSmemBytes = CG == 1 ? K4Cfg<1>::SMEM : K4Cfg<2>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (CG > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = unsigned(CG);
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   }
-  cudaError_t e = cudaFuncSetAttribute(k4_bf16x3, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
-  if (e != cudaSuccess) return e;
-  const int grid = int(tiles < num_sms ? tiles : num_sms);
-  k4_bf16x3<<<grid, K4_THREADS, K4_SMEM, stream>>>(tmy, tmx, p);
-  e = cudaGetLastError();
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  e = CG == 1 ? cudaLaunchKernelEx(&cfg, k4_bf16x3<1>, tmy, tmx, p) : cudaLaunchKernelEx(&cfg, k4_bf16x3<2>, tmy, tmx, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }
