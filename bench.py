@@ -286,14 +286,14 @@ def run_ours(args, cfg):
     hbm_bw = peaks.get("hbm_gbs", 6548.8) * 1e9
     flops = 8.0 * cfg.b * E                                  # 4 real MACs per complex MAC, b per estimate
     alg_bytes = 16 * E + 8 * cfg.T * cfg.K * cfg.N            # y read + h written + pilots
-    if sel in (ce.CE_KERNEL_TF32X3, ce.CE_KERNEL_BF16X3):
+    if sel in (ce.CE_KERNEL_TF32X3, ce.CE_KERNEL_BF16X3, ce.CE_KERNEL_BF16X3_PAIR):
         bf16 = peaks.get("bf16_tflops", 1605.7) * 1e12
         if sel == ce.CE_KERNEL_TF32X3:
             # TF32 = 1/2 bf16 (nominal ratio); 3 MMAs per product (hi/lo split)
             tc_peak, kname = bf16 * 0.5 / 3.0, "k3_tf32x3"
             src = "MEASURED_PEAKS bf16_tflops x 1/2 (tf32:bf16 nominal) / 3 (3xTF32 MMAs per product)"
         else:
-            tc_peak, kname = bf16 / 3.0, "k4_bf16x3"
+            tc_peak, kname = bf16 / 3.0, ("k4_bf16x3" if sel == ce.CE_KERNEL_BF16X3 else "k5_pair")
             src = "MEASURED_PEAKS bf16_tflops / 3 (BF16x3 MMAs per product)"
         t_tc, t_hbm = flops / tc_peak, alg_bytes / hbm_bw
         if t_tc >= t_hbm:
@@ -330,7 +330,7 @@ def run_ours(args, cfg):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded workload generator, SURVEY.md §8(d) recipe)",
             "config": _cfg_json(cfg, {"l2": f"rotating {nbuf} y/h buffer pairs ({nbuf * step_bytes / 2**20:.0f} MiB > L2)",
-                                      "kernel": {0: "auto", 1: "simt", 2: "tf32x3", 3: "bf16x3"}[args.kernel] + f"->{kname}",
+                                      "kernel": {0: "auto", 1: "simt", 2: "tf32x3", 3: "bf16x3", 4: "bf16x3_pair"}[args.kernel] + f"->{kname}",
                                       "global_batch_instances": world * cfg.T,
                                       "parallelism": f"antenna/batch shard x{world}"}),
             "roofline": roof,
@@ -356,7 +356,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 simt, 2 tf32x3, 3 bf16x3")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 simt, 2 tf32x3, 3 bf16x3, 4 bf16x3_pair")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ref-antennas", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)

@@ -60,7 +60,9 @@ typedef enum {
   CE_KERNEL_AUTO = 0,   /* library picks the fastest kernel meeting the 1e-4 parity bar */
   CE_KERNEL_SIMT = 1,   /* K2: FP32 SIMT complex FMA contraction */
   CE_KERNEL_TF32X3 = 2, /* K3: tcgen05 kind::tf32, error-compensated hi/lo split (3 MMAs) */
-  CE_KERNEL_BF16X3 = 3  /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring */
+  CE_KERNEL_BF16X3 = 3, /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring */
+  CE_KERNEL_BF16X3_PAIR = 4 /* K5: K4's arithmetic on a CTA pair (cta_group::2, M = 256) with the filter
+                               half-bank resident in shared memory */
 } ce_kernel;
 
 typedef struct ce_handle ce_handle; /* opaque */
@@ -121,14 +123,16 @@ int ce_free(ce_handle *h);
 
 /* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value, or for a tensor-core
  * kernel when some window does not fit its tile (2*kept + (2*(o_w-a_w) mod 8) > 256).
- * CE_KERNEL_AUTO (default): BF16X3 when it fits and the call is launchable (K <= 32, N even,
- * every window start a_w even, 16-byte aligned y/x), else TF32X3 when it fits, else SIMT.
+ * CE_KERNEL_AUTO (default): BF16X3 when it fits and the call is launchable (K <= 32, N even, every window
+ * start a_w even, 16-byte aligned y/x), else TF32X3 when it fits, else SIMT.  BF16X3_PAIR is explicit only
+ * (it also needs the resident half-bank plus 3 input stages to fit in shared memory; measured slower than
+ * BF16X3 on configs 3-5).
  * All meet the 1e-4 parity bar.
- * An explicit BF16X3 is rejected here when a window start is odd, and by ce_estimate (CE_EINVAL)
- * when the call itself is not launchable. */
+ * An explicit BF16X3 / BF16X3_PAIR is rejected here when a window start is odd, and by ce_estimate
+ * (CE_EINVAL) when the call itself is not launchable for it. */
 int ce_set_kernel(ce_handle *h, int32_t kernel);
 
-/* The kernel the most recent ce_estimate launched (CE_KERNEL_SIMT / _TF32X3 / _BF16X3); before
+/* The kernel the most recent ce_estimate launched (CE_KERNEL_SIMT / _TF32X3 / _BF16X3 / _BF16X3_PAIR); before
  * the first estimate, the kernel AUTO/the setting prefers for this geometry. */
 int ce_selected_kernel(const ce_handle *h, int32_t *out);
 

@@ -138,7 +138,7 @@ int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
 
 extern "C" {
 
-const char *ce_version(void) { return "libce 0.3 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3, K4 tcgen05 bf16x3 + TMA)"; }
+const char *ce_version(void) { return "libce 0.3 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3, K4 tcgen05 bf16x3 + TMA, K5 cta-pair bf16x3 resident bank)"; }
 
 const char *ce_status_string(int status) {
   switch (status) {
@@ -267,12 +267,12 @@ int ce_free(ce_handle *h) {
 int ce_set_kernel(ce_handle *h, int32_t kernel) {
   if (h == nullptr) return fail(CE_EINVAL, "ce_set_kernel: NULL handle");
   if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT && kernel != CE_KERNEL_TF32X3 &&
-      kernel != CE_KERNEL_BF16X3)
+      kernel != CE_KERNEL_BF16X3 && kernel != CE_KERNEL_BF16X3_PAIR)
     return fail(CE_EINVAL, "ce_set_kernel: unknown kernel");
-  if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3) && !h->tf32_ok)
+  if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->tf32_ok)
     return fail(CE_EINVAL, "ce_set_kernel: tensor-core kernels need 2*kept + row alignment <= 256 for every window");
-  if (kernel == CE_KERNEL_BF16X3 && !h->even_starts)
-    return fail(CE_EINVAL, "ce_set_kernel: BF16X3 needs every window start a_w even (16-byte TMA boxes)");
+  if ((kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->even_starts)
+    return fail(CE_EINVAL, "ce_set_kernel: BF16X3 / BF16X3_PAIR need every window start a_w even (16-byte TMA boxes)");
   h->kernel = kernel;
   return CE_OK;
 }
@@ -353,8 +353,13 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
     k = !h->tf32_ok ? CE_KERNEL_SIMT : (ce::bf16x3_launchable(a) ? CE_KERNEL_BF16X3 : CE_KERNEL_TF32X3);
   if (k == CE_KERNEL_BF16X3 && !ce::bf16x3_launchable(a))
     return fail(CE_EINVAL, "ce_estimate: BF16X3 needs K <= 32, even N, even window starts, 16-byte aligned y/x");
+  if (k == CE_KERNEL_BF16X3_PAIR && !ce::pair_launchable(a))
+    return fail(CE_EINVAL, "ce_estimate: BF16X3_PAIR needs the BF16X3 conditions and the resident half bank "
+                           "plus 3 input stages in shared memory");
   cudaError_t e;
-  if (k == CE_KERNEL_BF16X3)
+  if (k == CE_KERNEL_BF16X3_PAIR)
+    e = ce::launch_contract_pair(a, h->d_bank16, h->d_bank16 + h->bank16_plane, st, &h->launches);
+  else if (k == CE_KERNEL_BF16X3)
     e = ce::launch_contract_bf16x3(a, h->d_bank16, h->d_bank16 + h->bank16_plane, st, &h->launches);
   else if (k == CE_KERNEL_TF32X3)
     e = ce::launch_contract_tf32x3(a, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches);

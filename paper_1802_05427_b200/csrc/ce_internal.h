@@ -59,6 +59,11 @@ cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets,
 cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches);
 
+// K5: K4 on a CTA pair with the half bank resident in shared memory.
+bool pair_launchable(const ContractArgs &a);
+cudaError_t launch_contract_pair(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
+                                 cudaStream_t stream, int64_t *launches);
+
 void set_last_error(const std::string &msg);
 
 }  // namespace ce

@@ -37,6 +37,7 @@
 
 #include "ce_internal.h"
 #include "tc_ptx.cuh"
+#include "tmap.cuh"
 
 namespace ce {
 namespace {
@@ -60,7 +61,10 @@ constexpr int CK = 16;                     // complex per K chunk = 32 bf16 = 64
 constexpr int TM = 128;                    // A rows (columns c) per CTA
 constexpr int NMAXW = 256;                 // MMA N max (2*kept + row alignment)
 constexpr int KMAX = 32;                   // pilot rows per raw stage (K <= 32)
-constexpr int S_RAW = 3;                   // raw y/x stages
+#ifndef K4_S_RAW
+#define K4_S_RAW 4
+#endif
+constexpr int S_RAW = K4_S_RAW;            // raw y/x stages
 constexpr int A_PLANE = TM * 64;           // 8 KB
 constexpr int RAWY = TM * CK * 8;          // 16 KB
 constexpr int RAWX = KMAX * CK * 8;        // 4 KB
@@ -98,6 +102,7 @@ struct Tile4 {
 
 __device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank, int CG) {
   Tile4 ti;
+  // column block fastest (measured faster than window-fastest on configs 3-5)
   const int ctg = g % p.n_ctg;
   const int rest = g / p.n_ctg;
   const int w = rest % p.n_win;
@@ -208,7 +213,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     pdl_launch_dependents();          // the next kernel in the stream may launch (it waits for our exit)
     K4TR(2);
   }
-  pdl_wait();                         // the previous kernel's writes are visible from here on
+  // Programmatic dependent launch: every role that touches caller data (y, x, set_of_instance, h) waits
+  // for the previous kernel in the stream first.  The B producer without a set table reads only the
+  // filter bank, which ce_build_filters completed (stream-synchronised) before any estimate could be
+  // enqueued, so its first chunks are fetched while the previous kernel drains.
+#ifndef K4_NO_PDL
+  if (!(warp == 14 && p.soi == nullptr)) pdl_wait();
+#endif
   const int nks_total = (2 * p.b + 15) / 16;   // 16-element (bf16) MMA K steps over 2b
 
   if (warp == 12) {
@@ -467,61 +478,6 @@ __global__ void k4_build_bank(const float2 *__restrict__ W, int b, int nkc, int 
   }
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(2) * N * 4};
-  cuuint32_t box[2] = {cuuint32_t(2 * CK), cuuint32_t(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// Tensor maps are a pure function of (pointer, N, rows, box rows): cache the last few per host thread so
-// back-to-back calls on the same buffers skip the driver encode.
-struct MapCacheEntry {
-  const void *ptr;
-  int N, box_rows;
-  long long rows;
-  CUtensorMap map;
-};
-bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
-  constexpr int NC = 16;
-  static thread_local MapCacheEntry cache[NC];
-  static thread_local int used = 0, next = 0;
-  for (int i = 0; i < used; ++i)
-    if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows) {
-      *m = cache[i].map;
-      return true;
-    }
-  if (!make_map(m, ptr, N, rows, box_rows)) return false;
-  MapCacheEntry &e = cache[next];
-  e = MapCacheEntry{ptr, N, box_rows, rows, *m};
-  next = (next + 1) % NC;
-  if (used < NC) ++used;
-  return true;
-}
-
 // Per-device launch facts: smem attributes set once, SM count, and how many CTA pairs can be resident
 // at once (a pair needs two free SMs of one TPC).
 struct DevInfo {
@@ -643,9 +599,11 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   int na = 0;
+#ifndef K4_NO_PDL
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
+#endif
   if (CG > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
     at[na].val.clusterDim.x = unsigned(CG);

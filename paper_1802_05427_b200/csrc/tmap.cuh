@@ -1,0 +1,66 @@
+// Host-side TMA tensor-map helpers shared by the tcgen05 contraction kernels (K4, K5).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ce {
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(2) * N * 4};
+  cuuint32_t box[2] = {cuuint32_t(32), cuuint32_t(box_rows)};   // 16 complex per box row
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor maps are a pure function of (pointer, N, rows, box rows): cache the last few per host thread so
+// back-to-back calls on the same buffers skip the driver encode.
+struct MapCacheEntry {
+  const void *ptr;
+  int N, box_rows;
+  long long rows;
+  CUtensorMap map;
+};
+bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
+  constexpr int NC = 16;
+  static thread_local MapCacheEntry cache[NC];
+  static thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i)
+    if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows) {
+      *m = cache[i].map;
+      return true;
+    }
+  if (!make_map(m, ptr, N, rows, box_rows)) return false;
+  MapCacheEntry &e = cache[next];
+  e = MapCacheEntry{ptr, N, box_rows, rows, *m};
+  next = (next + 1) % NC;
+  if (used < NC) ++used;
+  return true;
+}
+
+}  // namespace
+}  // namespace ce

@@ -22,7 +22,7 @@ def _ce():
     return ce
 
 
-KERNELS = [1, 2, 3]       # CE_KERNEL_SIMT (K2), CE_KERNEL_TF32X3 (K3), CE_KERNEL_BF16X3 (K4)
+KERNELS = [1, 2, 3, 4]    # CE_KERNEL_SIMT (K2), _TF32X3 (K3), _BF16X3 (K4), _BF16X3_PAIR (K5)
 
 
 def _estimator(N, b, s, r, s2, kernel):
@@ -33,8 +33,9 @@ def _estimator(N, b, s, r, s2, kernel):
             ce.ce_set_kernel(est.handle, kernel)
         except ce.CEError as e:
             est.close()
-            if e.status == ce.CE_EINVAL and kernel in (ce.CE_KERNEL_TF32X3, ce.CE_KERNEL_BF16X3):
-                pytest.skip("window too wide for the K3 tile (2*kept > 256)")
+            if e.status == ce.CE_EINVAL and kernel in (ce.CE_KERNEL_TF32X3, ce.CE_KERNEL_BF16X3,
+                                                       ce.CE_KERNEL_BF16X3_PAIR):
+                pytest.skip("tensor-core kernel not applicable (2*kept > 256 or odd window starts)")
             raise
     return est.build()
 
@@ -247,18 +248,19 @@ def test_mse_gain_on_gpu(kernel):
 
 
 def test_kernels_agree_and_auto():
-    """K2 (FP32 SIMT), K3 (3xTF32) and K4 (BF16x3) agree far inside the oracle tolerance;
-    AUTO launches K4 when it is launchable and falls back to K3 when it is not."""
+    """K2 (FP32 SIMT), K3 (3xTF32), K4 (BF16x3) and K5 (BF16x3 CTA pair) agree far inside the oracle
+    tolerance; AUTO launches K4 when it is launchable and falls back to K3 when it is not."""
     ce = _ce()
     cfg = CONFIGS[3]
     r, s2, x, y, soi = _inputs(cfg)
     h1 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=1)
     h2 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=2)
     h3 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=3)
+    h4 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=4)
     h0 = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=0)
-    for h in (h2, h3):
+    for h in (h2, h3, h4):
         assert oracle.rel_fro_error_per_instance(h, h1.astype(np.complex128)).max() < 2e-5
-    assert np.array_equal(h0.view(np.float32), h3.view(np.float32))
+    assert np.array_equal(h0.view(np.float32), h3.view(np.float32))      # AUTO launches K4 here
     # misaligned (8-byte) y: K4 is not launchable -> AUTO falls back to K3; explicit K4 -> EINVAL
     est = _estimator(cfg.N, cfg.b, cfg.stride, r, s2, None)
     buf = torch.empty(y.size + 1, dtype=torch.complex64, device="cuda")

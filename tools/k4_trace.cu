@@ -12,6 +12,7 @@
 #include "../include/ce.h"
 
 extern "C" int ce_k4_trace_set(void *dptr);
+extern "C" int ce_k5_trace_set(void *dptr);
 
 int main(int argc, char **argv) {
   int N = argc > 1 ? atoi(argv[1]) : 1200, b = argc > 2 ? atoi(argv[2]) : 100, s = argc > 3 ? atoi(argv[3]) : 100;
@@ -61,6 +62,7 @@ int main(int argc, char **argv) {
   ce_selected_kernel(h, &sel);
   printf("kernel %d: %.2f us per call (untraced, back-to-back)\n", sel, 1e3 * ms / reps);
   ce_k4_trace_set(dtr);
+  ce_k5_trace_set(dtr);
   for (int i = 0; i < 3; ++i) {
     ce_estimate(h, dy[i % NB], dx, dh[i % NB], T, M, K, nullptr, nullptr);
     cudaDeviceSynchronize();
@@ -99,7 +101,7 @@ int main(int argc, char **argv) {
       if (slot >= 8 && slot < 32) snprintf(buf, 64, "raw TMA issue it=%d", slot - 8);
       else if (slot >= 32 && slot < 56) snprintf(buf, 64, "raw full seen it=%d", slot - 32);
       else if (slot >= 56 && slot < 80) snprintf(buf, 64, "A written it=%d", slot - 56);
-      else if (slot >= 80 && slot < 104) snprintf(buf, 64, "B issue it=%d", slot - 80);
+      else if (slot >= 80 && slot < 104) snprintf(buf, 64, "B issue/fwd it=%d", slot - 80);
       else if (slot >= 104 && slot < 128) snprintf(buf, 64, "MMA issue it=%d", slot - 104);
       else if (slot >= 128 && slot < 136) snprintf(buf, 64, "tile MMAs committed lt=%d", slot - 128);
       else if (slot >= 136 && slot < 144) snprintf(buf, 64, "epi start lt=%d", slot - 136);
