@@ -16,10 +16,10 @@
 //
 // Pipeline (persistent, one CTA per SM, 480 threads):
 //   warp 12   : raw producer -- 2D TMA of the raw y box [128 rows x 16 complex] and the pilot box
-//               [K rows x 16 complex] of each K chunk into a 3-deep raw ring
-//   warps 0-7 : transform -- LS factors f = conj(x)/|x|^2 once per (k, j) in place in the raw pilot
-//               slot (named barrier), then LS = y f -> bf16 hi/lo -> SWIZZLE_64B K-major A tiles of the
-//               3-deep A/B ring; fence.proxy.async; arrive a_full
+//               [K rows x 16 complex] of each K chunk into a 4-deep raw ring
+//   warps 0-7 : transform -- y and x of 4 rows x 2 tones per thread into registers, LS = y conj(x)/|x|^2,
+//               release the raw slot, bf16 hi/lo -> SWIZZLE_64B K-major A tiles of the 3-deep A/B ring;
+//               fence.proxy.async; arrive a_full
 //   warp 14   : B producer -- cp.async.bulk of this CTA's rows of the bf16 hi/lo bank chunk
 //               (pre-swizzled SW64 image)
 //   warp 13   : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> st_empty;
@@ -256,42 +256,46 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
         if (tid == 0 && it < 24) K4TR(32 + it);
         const float4 *ry = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE);
-        float4 *rx = reinterpret_cast<float4 *>(raw + sr * RAW_STAGE + RAWY);
-        // LS factors in place: f = conj(x) / |x|^2 for the K x 16 pilots of this chunk
-        if (tid < p.K * 8) {
-          const float4 xv = rx[tid];
-          const float i0 = rcp_approx(xv.x * xv.x + xv.y * xv.y);
-          const float i1 = rcp_approx(xv.z * xv.z + xv.w * xv.w);
-          const bool ok0 = kc * CK + 2 * (tid & 7) < p.b, ok1 = kc * CK + 2 * (tid & 7) + 1 < p.b;
-          rx[tid] = make_float4(ok0 ? xv.x * i0 : 0.f, ok0 ? -xv.y * i0 : 0.f, ok1 ? xv.z * i1 : 0.f,
-                                ok1 ? -xv.w * i1 : 0.f);   // zero factor masks the K tail (j >= b)
+        const float4 *rx = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE + RAWY);
+        float4 yv[4], xv[4];
+        int xr = x_first;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {          // all 8 loads in flight at once
+          yv[i] = ry[(rb + 32 * i) * 8 + jp];
+          xv[i] = rx[xr * 8 + jp];
+          xr += x_step;
+          if (xr >= p.K) xr -= p.K;
         }
-        named_bar_sync(1, NTR);
+        // LS = y / x = y conj(x) / |x|^2 per element; a zero factor masks the K tail (j >= b)
+        const bool ok0 = kc * CK + 2 * jp < p.b, ok1 = kc * CK + 2 * jp + 1 < p.b;
+        uint32_t hv[4][2], lv[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float i0 = ok0 ? rcp_approx(xv[i].x * xv[i].x + xv[i].y * xv[i].y) : 0.f;
+          const float i1 = ok1 ? rcp_approx(xv[i].z * xv[i].z + xv[i].w * xv[i].w) : 0.f;
+          const float f0r = xv[i].x * i0, f0i = -xv[i].y * i0, f1r = xv[i].z * i1, f1i = -xv[i].w * i1;
+          const float l0r = yv[i].x * f0r - yv[i].y * f0i, l0i = yv[i].x * f0i + yv[i].y * f0r;
+          const float l1r = yv[i].z * f1r - yv[i].w * f1i, l1i = yv[i].z * f1i + yv[i].w * f1r;
+          hv[i][0] = pack_bf16(l0r, l0i);
+          hv[i][1] = pack_bf16(l1r, l1i);
+          lv[i][0] = pack_bf16(l0r - bf16_lo_f(hv[i][0]), l0i - bf16_hi_f(hv[i][0]));
+          lv[i][1] = pack_bf16(l1r - bf16_lo_f(hv[i][1]), l1i - bf16_hi_f(hv[i][1]));
+        }
+        mbar_arrive(&raw_empty[sr]);           // the raw slot is consumed (values used above): refill it
         mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
         uint8_t *ah = ab + sa * AB_STAGE;
         uint8_t *al = ah + A_PLANE;
-        int xr = x_first;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = rb + 32 * i;
-          const float4 yv = ry[r * 8 + jp];
-          const float4 fv = rx[xr * 8 + jp];
-          const float l0r = yv.x * fv.x - yv.y * fv.y, l0i = yv.x * fv.y + yv.y * fv.x;
-          const float l1r = yv.z * fv.z - yv.w * fv.w, l1i = yv.z * fv.w + yv.w * fv.z;
-          const uint32_t h0 = pack_bf16(l0r, l0i), h1 = pack_bf16(l1r, l1i);
-          const uint32_t g0 = pack_bf16(l0r - bf16_lo_f(h0), l0i - bf16_hi_f(h0));
-          const uint32_t g1 = pack_bf16(l1r - bf16_lo_f(h1), l1i - bf16_hi_f(h1));
           // SW64 K-major: row r at r*64 bytes, 16-byte chunk (jp>>1) ^ ((r>>1)&3), 8-byte half (jp&1)
           const int off = r * 64 + ((((jp >> 1) ^ ((r >> 1) & 3))) << 4) + ((jp & 1) << 3);
-          *reinterpret_cast<uint2 *>(ah + off) = make_uint2(h0, h1);
-          *reinterpret_cast<uint2 *>(al + off) = make_uint2(g0, g1);
-          xr += x_step;
-          if (xr >= p.K) xr -= p.K;
+          *reinterpret_cast<uint2 *>(ah + off) = make_uint2(hv[i][0], hv[i][1]);
+          *reinterpret_cast<uint2 *>(al + off) = make_uint2(lv[i][0], lv[i][1]);
         }
         fence_proxy_async();
         if (tid == 0 && it < 24) K4TR(56 + it);
         mbar_arrive(&a_full[sa]);
-        mbar_arrive(&raw_empty[sr]);
       }
     }
   } else if (warp < 12) {
@@ -330,7 +334,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
             float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
             float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
             if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
+#ifdef K4_EXP_NOSTORE
+            if (c0 < 0) hrow[ci] = a0;
+#else
             if (c0 < p.cols) hrow[ci] = a0;
+#endif
             if (c0 + 8 < p.cols) hrow[row8 + ci] = a1;
             if (c0 + 16 < p.cols) hrow[2 * row8 + ci] = a2;
             if (c0 + 24 < p.cols) hrow[3 * row8 + ci] = a3;
@@ -358,6 +366,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
+#ifdef K4_EXP_BONCE
+          if (it >= S_AB) { mbar_arrive(&b_full[s]); continue; }
+#endif
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
           const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * rows) * 32;   // bf16 elements

@@ -109,6 +109,53 @@ __global__ void copyk(const __grid_constant__ CUtensorMap tm, float *dst, long l
   }
 }
 
+// K4 read pattern: tile g -> (t, w, ct) by `order`; each tile reads nkc boxes [128 rows][16 complex] at
+// columns 2(a_w + 16 kc) of rows t*cols + ct*128.  order 0: ct fastest; 1: w fastest; 2: kc-outer
+// (all tiles of a CTA interleaved per chunk is not modelled).
+__global__ void k4pat(const __grid_constant__ CUtensorMap tm, int T, int n_win, int n_ct, int b, int s_stride,
+                      int cols, int nkc, int stages, int order, unsigned long long *sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bars[16];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int n_tiles = T * n_win * n_ct;
+  const int total = ((n_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)) * nkc;
+  auto coords = [&](int j, int *c0, int *c1) {
+    const int tile = blockIdx.x + (j / nkc) * gridDim.x, kc = j % nkc;
+    int t, w, ct;
+    if (order == 0) { ct = tile % n_ct; w = (tile / n_ct) % n_win; t = tile / (n_ct * n_win); }
+    else { w = tile % n_win; ct = (tile / n_win) % n_ct; t = tile / (n_ct * n_win); }
+    const int a = min(w * s_stride, 2 * 1638 - b);   // N = 3276 for this bench tensor
+    *c0 = 2 * (a + 16 * kc);
+    *c1 = t * cols + ct * 128;
+  };
+  auto issue = [&](int j, int s) {
+    int c0, c1;
+    coords(j, &c0, &c1);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[s])), "r"(16384u) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(sm + size_t(s) * 16384)),
+        "l"(reinterpret_cast<uint64_t>(&tm)), "r"(c0), "r"(c1), "r"(smem_u32(&bars[s]))
+        : "memory");
+  };
+  unsigned long long acc = 0;
+  int next = 0;
+  for (int s = 0; s < stages && next < total; ++s, ++next) issue(next, s);
+  for (int j = 0; j < total; ++j) {
+    const int s = j % stages;
+    asm volatile(
+        "{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(
+            smem_u32(&bars[s])),
+        "r"((j / stages) & 1)
+        : "memory");
+    acc += sm[size_t(s) * 16384 + 7];
+    if (next < total) issue(next++, s);
+  }
+  sink[blockIdx.x] = acc;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -129,6 +176,33 @@ int main(int argc, char **argv) {
   unsigned long long *sink;
   cudaMalloc(&sink, 4096 * 8);
   cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  {
+    // K4 config-5 read pattern on the first T=2 instances (rows = T * 6144)
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
+    cuuint64_t str[1] = {cuuint64_t(2) * N * 4};
+    cuuint32_t box[2] = {32, 128}, es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cudaFuncSetAttribute(k4pat, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaEvent_t c0, c1;
+    cudaEventCreate(&c0);
+    cudaEventCreate(&c1);
+    for (int Tn : {2, 20})
+      for (int order : {0, 1})
+        for (int st : {3, 4, 8}) {
+          k4pat<<<nsm, 32, st * 16384>>>(tm, Tn, 26, 48, 126, 126, 6144, 8, st, order, sink);
+          cudaEventRecord(c0);
+          k4pat<<<nsm, 32, st * 16384>>>(tm, Tn, 26, 48, 126, 126, 6144, 8, st, order, sink);
+          cudaEventRecord(c1);
+          cudaEventSynchronize(c1);
+          float ms;
+          cudaEventElapsedTime(&ms, c0, c1);
+          const double moved = double(Tn) * 26 * 48 * 8 * 16384;
+          printf("K4PAT T=%d order %d stages %d: %.1f us  %.1f GB/s  %s\n", Tn, order, st, ms * 1e3, moved / ms / 1e6,
+                 cudaGetErrorString(cudaGetLastError()));
+        }
+  }
   float *dcopy;
   cudaMalloc(&dcopy, bytes);
   cudaFuncSetAttribute(copyk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
