@@ -22,3 +22,14 @@ from .lmmse import (  # noqa: F401
     toeplitz_hermitian,
     window_table,
 )
+from .comb import (  # noqa: F401
+    comb_estimate,
+    comb_filters,
+    comb_full_lmmse,
+    comb_geometry,
+    comb_ls,
+    comb_mse_per_tone,
+    comb_out_tones,
+    rect_filter,
+    zoh_fill,
+)

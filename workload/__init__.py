@@ -10,7 +10,7 @@ block apply).  It only draws the inputs the estimator consumes:
 Recipe: SURVEY.md §8(d) "Synthetic inputs" and the readings A3/A4/A6/A12 of
 SURVEY.md §8(c), restated in DESIGN.md §3.
 """
-from .configs import CONFIGS, Config, get_config  # noqa: F401
+from .configs import COMB_CONFIGS, CONFIGS, CombConfig, Config, get_comb_config, get_config  # noqa: F401
 from .gen import (  # noqa: F401
     channel_stats,
     gen_instances,
@@ -19,3 +19,4 @@ from .gen import (  # noqa: F401
     rms_spread_taps,
     set_of_instance,
 )
+from .comb import comb_instances, comb_pilots, comb_stats, comb_true_stats  # noqa: F401,E402

@@ -75,3 +75,54 @@ def get_config(cfg) -> Config:
                 return c
         return CONFIGS[int(cfg)]
     return CONFIGS[int(cfg)]
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-1: the paper's comb-pilot grouped estimators (3W / 12W-LMMSE, Tables I-II).
+# Channel per Table III: 6 taps at delays 0..5 samples (Nfft rate) with powers
+# [-2, -8, -10, -12, -15, -18] dB.  The estimator uses the paper's FIXED design: r_d of Eq. eqrd with
+# the assumed path count L (reading A5: normalised by Nfft) and SNR_fixed
+# (Table III: L = 8, 40 dB).
+# ------------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class CombConfig:
+    name: str
+    M: int                 # BS antennas (paper's R)
+    S: int                 # comb spacing = pilot-interleaved UE slots (12 in Fig. fig1)
+    n_ue: int              # active UEs estimated (the first n_ue comb offsets; 4 in Table III)
+    N: int
+    Nfft: int
+    T: int                 # estimation instances (slots)
+    G: int                 # pilots per group window (12 -> 12W, 3 -> 3W)
+    mode: str              # "full" (12W: every tone) or "sub" (3W: G tones per group, then ZOH)
+    tap_delays: Tuple[float, ...] = (0, 1, 2, 3, 4, 5)
+    tap_db: Tuple[float, ...] = (-2, -8, -10, -12, -15, -18)
+    snr_db: float = 25.0   # true SNR of the synthetic channel
+    L_assumed: float = 8.0
+    snr_fixed_db: float = 40.0
+
+    @property
+    def K(self) -> int:
+        return self.N // self.S
+
+    @property
+    def estimates(self) -> int:
+        return self.T * self.M * self.n_ue * self.N
+
+
+COMB_CONFIGS = {
+    "comb_tiny12": CombConfig("comb_tiny12", M=4, S=4, n_ue=4, N=96, Nfft=128, T=2, G=4, mode="full",
+                              tap_delays=(0, 1, 2), tap_db=(-1, -6, -9), snr_db=10.0, L_assumed=4.0,
+                              snr_fixed_db=20.0),
+    "comb_tiny3": CombConfig("comb_tiny3", M=3, S=6, n_ue=3, N=96, Nfft=128, T=2, G=3, mode="sub",
+                             tap_delays=(0, 1, 2), tap_db=(-1, -6, -9), snr_db=10.0, L_assumed=4.0,
+                             snr_fixed_db=20.0),
+    "paper_12w": CombConfig("paper_12w", M=16, S=12, n_ue=4, N=1200, Nfft=2048, T=18, G=12, mode="full"),
+    "paper_3w": CombConfig("paper_3w", M=16, S=12, n_ue=4, N=1200, Nfft=2048, T=18, G=3, mode="sub"),
+    "massive_12w": CombConfig("massive_12w", M=128, S=12, n_ue=12, N=1200, Nfft=2048, T=20, G=12,
+                              mode="full"),
+}
+
+
+def get_comb_config(name) -> CombConfig:
+    return name if isinstance(name, CombConfig) else COMB_CONFIGS[name]
