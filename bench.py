@@ -349,6 +349,100 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_comb(args):
+    """--comb NAME: the paper's comb-pilot 3W / 12W-LMMSE path (NEXT-1, K6) on one of workload.COMB_CONFIGS."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_05427_b200 as ce
+    from paper_1802_05427_b200.shard import antenna_shard
+
+    world, rank, local = _dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload.get_comb_config(args.comb)
+    r, s2 = workload.comb_stats(cfg)
+    x = workload.comb_pilots(cfg)
+    m_lo, m_hi = antenna_shard(world * cfg.M, world, rank)
+    y = workload.comb_instances(cfg, x=x, m_lo=m_lo, m_hi=m_hi)
+    est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    T, M, N = y.shape
+    out_bytes = T * M * cfg.n_ue * N * 8
+    nbuf = max(2, int(np.ceil(1.25 * L2_BYTES / (y.nbytes + out_bytes))) + 1)
+    y_dev = [torch.from_numpy(y).to(dev) for _ in range(nbuf)]
+    h_dev = [torch.empty((T, M, cfg.n_ue, N), dtype=torch.complex64, device=dev) for _ in range(nbuf)]
+    x_dev = torch.from_numpy(x).to(dev)
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        est.estimate(y_dev[i % nbuf], x_dev, out=h_dev[i % nbuf])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = est.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            est.estimate(y_dev[i % nbuf], x_dev, out=h_dev[i % nbuf])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = est.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    E = cfg.estimates
+    value = world * E * args.steps / (ms_max * 1e-3)
+    kernel_s = ms / args.steps * 1e-3
+    # end to end: pinned host y -> device, estimate, device -> pinned host h, every step
+    y_pin = torch.from_numpy(y).pin_memory()
+    h_pin = torch.empty((T, M, cfg.n_ue, N), dtype=torch.complex64).pin_memory()
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        yd = y_pin.to(dev, non_blocking=True)
+        hd = est.estimate(yd, x_dev)
+        h_pin.copy_(hd, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * E * e2e_steps / (float(e2e_ms.item()) * 1e-3)
+    peaks = _peaks()
+    hbm_bw = peaks.get("hbm_gbs", 6548.8) * 1e9
+    alg_bytes = out_bytes + y.nbytes + x.nbytes
+    roof = {"bound": "hbm", "achieved": alg_bytes / kernel_s / 1e9, "peak": hbm_bw / 1e9, "unit": "GB/s",
+            "frac": alg_bytes / kernel_s / hbm_bw, "peak_source": "MEASURED_PEAKS hbm_gbs", "traffic": None,
+            "kernel": "k6_estimate", "kernel_us": kernel_s * 1e6, "algorithmic_bytes_per_launch": alg_bytes,
+            "algorithmic_flops_per_launch": 8.0 * cfg.G * E}
+    if rank == 0:
+        line = {
+            "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value, "unit": "estimates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (workload.comb: Table III channel, fixed-design r_d / SNR_fixed)",
+            "config": {"workload": f"comb_{cfg.name}_{cfg.M}x{cfg.n_ue}of{cfg.S}x{cfg.N}_T{cfg.T}_G{cfg.G}_{cfg.mode}",
+                       "M": cfg.M, "S": cfg.S, "n_ue": cfg.n_ue, "N": cfg.N, "T": cfg.T, "G": cfg.G,
+                       "mode": cfg.mode, "l2": f"rotating {nbuf} y/h buffer pairs (> L2)",
+                       "parallelism": f"antenna shard x{world}"},
+            "roofline": roof, "cpu_baseline": None,
+            "e2e": {"value": e2e_value, "unit": "estimates/s", "h2d_bytes_per_step": int(y.nbytes),
+                    "d2h_bytes_per_step": int(out_bytes), "steps": e2e_steps},
+            "gpu_launches": int(launches), "clocks": clk.summary(), "device": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    est.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,9 +455,15 @@ def main():
     ap.add_argument("--ref-antennas", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comb", default=None, help="run the comb-pilot 3W/12W path on workload.COMB_CONFIGS[NAME]")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.comb:
+        if args.impl == "reference":
+            raise SystemExit("--impl reference times the block path's oracle; use it without --comb")
+        run_comb(args)
+        return
     cfg = workload.get_config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -149,6 +149,53 @@ int ce_window_table(int32_t N, int32_t b, int32_t stride, int32_t *out, int32_t 
 /* Number of CUDA kernels this handle has launched (K1 + K2/K3), for launch accounting. */
 int ce_launch_count(const ce_handle *h, int64_t *out);
 
+/* ---------------------------------------------------------------------------------------------------
+ * NEXT-1: the paper's own comb-pilot grouped estimators, 3W-LMMSE and 12W-LMMSE (PAPER.md:345-403,
+ * Tables I-II; zero-order hold of PAPER.md:519).  UE s (0-based) owns pilot tones S*j + s, j < K = N/S
+ * (Eq. 6).  Group g in [0, K) uses the pilot window [a_g, a_g + G),
+ * a_g = clamp(g - (G-1)/2, 0, K - G), and weight type g - a_g; its weight is
+ *   W = R[out, in] (R[in, in] + sigma^2 I)^-1     (Eq. 17, R[p, q] = r[p - q], r[-d] = conj(r[d]))
+ * CE_COMB_FULL (12W): group g outputs the S tones S*g + q (every tone); one weight set per UE.
+ * CE_COMB_SUB  (3W):  group g outputs the G tones S*g + s + (S/G) q; weights shared by all UEs; every
+ *                     other tone holds the last estimate at or before it (the first estimate before it).
+ * Readings C1-C4 in DESIGN.md.
+ * ------------------------------------------------------------------------------------------------- */
+typedef enum { CE_COMB_FULL = 0, CE_COMB_SUB = 1 } ce_comb_mode;
+
+typedef struct ce_comb_handle ce_comb_handle; /* opaque */
+
+typedef struct {
+  int32_t N;      /* used subcarriers, N % S == 0 */
+  int32_t S;      /* comb spacing: pilot-interleaved UE slots (12 in PAPER.md Fig. fig1) */
+  int32_t n_ue;   /* UEs estimated: comb offsets 0 .. n_ue-1, 1 <= n_ue <= S */
+  int32_t G;      /* pilots per group window, 1 <= G <= min(N/S, 32); SUB needs S % G == 0 */
+  int32_t mode;   /* ce_comb_mode; FULL needs S <= 64 */
+  const double *r_hh; /* host [N][2] complex128 first column of R_hh (same statistics for all UEs); copied */
+  double sigma2;      /* sigma^2 / sigma_s^2 > 0 */
+} ce_comb_params;
+
+/* Validate, copy the statistics to the current device, allocate the weights.  CE_EINVAL / CE_ENODEV /
+ * CE_ENOMEM as ce_init. */
+int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out);
+/* K6a: FP64 Cholesky build of every (UE, type) weight, rounded to complex64; synchronises the stream
+ * once to read the positive-definite flag (CE_ENOTPD). */
+int ce_comb_build_filters(ce_comb_handle *h, void *stream);
+/* K6b hot path on device pointers, asynchronous on `stream`:
+ *   d_y : complex64 [T][M][N]     received pilot OFDM symbol of each antenna (all UEs on their combs)
+ *   d_x : complex64 [T][N]        comb pilot symbol: tone k carries UE (k % S)'s pilot
+ *   d_h : complex64 [T][M][n_ue][N] estimates (caller-owned, must not alias d_y / d_x)
+ * CE_ESTATE before a successful build; CE_EINVAL for NULL / misaligned (8 B) pointers, T or M < 1,
+ * aliasing. */
+int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *d_h, int32_t T, int32_t M,
+                     void *stream);
+/* Copy the weights to host: complex64 [n_w][G types][n_out][G], n_w = n_ue (FULL) or 1 (SUB),
+ * n_out = S (FULL) or G (SUB).  Synchronous. */
+int ce_comb_get_filters(ce_comb_handle *h, void *host_W);
+/* Kernels launched by this handle (K6a + K6b). */
+int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out);
+/* Free; NULL allowed. */
+int ce_comb_free(ce_comb_handle *h);
+
 /* Static description of a status code; never NULL. */
 const char *ce_status_string(int status);
 

@@ -4,6 +4,8 @@ The product path: libce.so (include/ce.h; CUDA kernels for sm_100a) behind a thi
 ctypes binding with the same function names.  No CPU fallback, no oracle import.
 """
 from .ce import (  # noqa: F401
+    CE_COMB_FULL,
+    CE_COMB_SUB,
     CE_EINVAL,
     CE_ENODEV,
     CE_ENOMEM,
@@ -18,7 +20,12 @@ from .ce import (  # noqa: F401
     EXPORTED,
     CEError,
     ChannelEstimator,
+    CombEstimator,
     ce_build_filters,
+    ce_comb_build_filters,
+    ce_comb_estimate,
+    ce_comb_free,
+    ce_comb_init,
     ce_estimate,
     ce_estimate_host,
     ce_free,

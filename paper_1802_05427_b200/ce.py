@@ -29,7 +29,9 @@ CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3, CE_KERNEL_BF16X3, CE_KERNEL_BF
 EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
             "ce_selected_kernel",
             "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
-            "ce_version")
+            "ce_version", "ce_comb_init", "ce_comb_build_filters", "ce_comb_estimate", "ce_comb_get_filters",
+            "ce_comb_launch_count", "ce_comb_free")
+CE_COMB_FULL, CE_COMB_SUB = 0, 1
 
 
 class ce_params(ctypes.Structure):
@@ -37,7 +39,18 @@ class ce_params(ctypes.Structure):
                 ("r_hh", POINTER(c_double)), ("sigma2", POINTER(c_double))]
 
 
+class ce_comb_params(ctypes.Structure):
+    _fields_ = [("N", c_int32), ("S", c_int32), ("n_ue", c_int32), ("G", c_int32), ("mode", c_int32),
+                ("r_hh", POINTER(c_double)), ("sigma2", c_double)]
+
+
 lib.ce_init.argtypes = [POINTER(ce_params), POINTER(c_void_p)]
+lib.ce_comb_init.argtypes = [POINTER(ce_comb_params), POINTER(c_void_p)]
+lib.ce_comb_build_filters.argtypes = [c_void_p, c_void_p]
+lib.ce_comb_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]
+lib.ce_comb_get_filters.argtypes = [c_void_p, c_void_p]
+lib.ce_comb_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
+lib.ce_comb_free.argtypes = [c_void_p]
 lib.ce_build_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]
 lib.ce_estimate_host.argtypes = lib.ce_estimate.argtypes
@@ -55,7 +68,8 @@ lib.ce_version.argtypes = []
 lib.ce_version.restype = c_char_p
 for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
            "ce_selected_kernel",
-           "ce_get_filters", "ce_window_table", "ce_launch_count"):
+           "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_comb_init", "ce_comb_build_filters",
+           "ce_comb_estimate", "ce_comb_get_filters", "ce_comb_launch_count", "ce_comb_free"):
     getattr(lib, _n).restype = c_int
 
 
@@ -224,6 +238,83 @@ class ChannelEstimator:
     def close(self):
         if getattr(self, "handle", None):
             ce_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ce_comb_init(N: int, S: int, n_ue: int, G: int, mode: int, r_hh, sigma2: float) -> int:
+    r = np.ascontiguousarray(np.asarray(r_hh, np.complex128).reshape(-1))
+    if r.shape[0] != N:
+        raise ValueError("r_hh must have N entries")
+    rv = r.view(np.float64)
+    p = ce_comb_params(N, S, n_ue, G, mode, rv.ctypes.data_as(POINTER(c_double)), float(sigma2))
+    h = c_void_p()
+    _check(lib.ce_comb_init(ctypes.byref(p), ctypes.byref(h)), "ce_comb_init")
+    return h.value
+
+
+def ce_comb_build_filters(h: int, stream: int = 0) -> None:
+    _check(lib.ce_comb_build_filters(h, c_void_p(stream)), "ce_comb_build_filters")
+
+
+def ce_comb_estimate(h: int, d_y: int, d_x: int, d_h: int, T: int, M: int, stream: int = 0) -> None:
+    _check(lib.ce_comb_estimate(h, c_void_p(d_y), c_void_p(d_x), c_void_p(d_h), T, M, c_void_p(stream)),
+           "ce_comb_estimate")
+
+
+def ce_comb_free(h: int) -> None:
+    _check(lib.ce_comb_free(h), "ce_comb_free")
+
+
+class CombEstimator:
+    """The paper's comb-pilot 3W / 12W-LMMSE (NEXT-1) on one device (libce ce_comb_* entry points).
+
+    est = CombEstimator(N, S, n_ue, G, mode, r_hh, sigma2).build()
+    h = est.estimate(y, x)     # y complex64 cuda [T][M][N], x [T][N] -> h [T][M][n_ue][N]
+    """
+
+    def __init__(self, N: int, S: int, n_ue: int, G: int, mode, r_hh, sigma2: float):
+        if isinstance(mode, str):
+            mode = {"full": CE_COMB_FULL, "sub": CE_COMB_SUB}[mode]
+        self.N, self.S, self.n_ue, self.G, self.mode = int(N), int(S), int(n_ue), int(G), int(mode)
+        self.handle = ce_comb_init(N, S, n_ue, G, mode, r_hh, sigma2)
+
+    def build(self, stream=None) -> "CombEstimator":
+        ce_comb_build_filters(self.handle, _stream_ptr(stream))
+        return self
+
+    def filters(self) -> np.ndarray:
+        n_w = self.n_ue if self.mode == CE_COMB_FULL else 1
+        n_out = self.S if self.mode == CE_COMB_FULL else self.G
+        out = np.empty((n_w, self.G, n_out, self.G), np.complex64)
+        _check(lib.ce_comb_get_filters(self.handle, out.ctypes.data), "ce_comb_get_filters")
+        return out
+
+    def estimate(self, y, x, out=None, stream=None):
+        import torch
+        if y.dtype != torch.complex64 or x.dtype != torch.complex64 or not (y.is_cuda and x.is_cuda):
+            raise TypeError("y and x must be complex64 CUDA tensors")
+        T, M, N = y.shape
+        if N != self.N or tuple(x.shape) != (T, N) or not (y.is_contiguous() and x.is_contiguous()):
+            raise ValueError(f"shape mismatch: y {tuple(y.shape)}, x {tuple(x.shape)}, N={self.N}")
+        if out is None:
+            out = torch.empty((T, M, self.n_ue, N), dtype=torch.complex64, device=y.device)
+        ce_comb_estimate(self.handle, y.data_ptr(), x.data_ptr(), out.data_ptr(), T, M, _stream_ptr(stream))
+        return out
+
+    def launch_count(self) -> int:
+        v = c_int64()
+        _check(lib.ce_comb_launch_count(self.handle, ctypes.byref(v)), "ce_comb_launch_count")
+        return v.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            ce_comb_free(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -94,3 +94,31 @@ def test_no_device_is_loud():
     except ImportError:
         pass
     assert _raw(72, 12, 12, 1) == ce.CE_ENODEV
+
+
+def test_comb_init_validation():
+    """ce_comb_init rejects bad geometry before touching CUDA (CE_EINVAL); valid params on a machine
+    without a GPU are CE_ENODEV."""
+    r = np.zeros(96, np.complex128)
+    r[0] = 1.0
+    bad = [dict(N=96, S=5, n_ue=1, G=2, mode=0),        # N % S != 0
+           dict(N=96, S=4, n_ue=5, G=2, mode=0),        # n_ue > S
+           dict(N=96, S=4, n_ue=1, G=25, mode=0),       # G > K
+           dict(N=96, S=4, n_ue=1, G=3, mode=1),        # sub mode needs S % G == 0
+           dict(N=96, S=4, n_ue=1, G=2, mode=7)]        # unknown mode
+    for kw in bad:
+        with pytest.raises(ce.CEError) as e:
+            ce.ce_comb_init(r_hh=r, sigma2=0.1, **kw)
+        assert e.value.status == ce.CE_EINVAL, kw
+    with pytest.raises(ce.CEError) as e:
+        ce.ce_comb_init(96, 4, 4, 4, 0, r, -1.0)
+    assert e.value.status == ce.CE_EINVAL
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        with pytest.raises(ce.CEError) as e:
+            ce.ce_comb_init(96, 4, 4, 4, 0, r, 0.1)
+        assert e.value.status == ce.CE_ENODEV

@@ -117,6 +117,8 @@ COMB_CONFIGS = {
     "comb_tiny3": CombConfig("comb_tiny3", M=3, S=6, n_ue=3, N=96, Nfft=128, T=2, G=3, mode="sub",
                              tap_delays=(0, 1, 2), tap_db=(-1, -6, -9), snr_db=10.0, L_assumed=4.0,
                              snr_fixed_db=20.0),
+    "comb_small12": CombConfig("comb_small12", M=9, S=12, n_ue=5, N=288, Nfft=512, T=2, G=12, mode="full"),
+    "comb_small3": CombConfig("comb_small3", M=5, S=12, n_ue=7, N=240, Nfft=512, T=2, G=3, mode="sub"),
     "paper_12w": CombConfig("paper_12w", M=16, S=12, n_ue=4, N=1200, Nfft=2048, T=18, G=12, mode="full"),
     "paper_3w": CombConfig("paper_3w", M=16, S=12, n_ue=4, N=1200, Nfft=2048, T=18, G=3, mode="sub"),
     "massive_12w": CombConfig("massive_12w", M=128, S=12, n_ue=12, N=1200, Nfft=2048, T=20, G=12,
