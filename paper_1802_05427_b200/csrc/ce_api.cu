@@ -34,6 +34,18 @@ bool window_table(int32_t N, int32_t b, int32_t s, std::vector<Window> *out) {
   return true;
 }
 
+// Tensor-core tiles hold at most 256 accumulator columns (2 * kept + row alignment <= 256): windows that
+// keep more outputs are split into output sub-windows over the same LS input range (same a_w, b), each
+// keeping <= 124 consecutive outputs.  Reading the full b-wide input per sub-window re-reads y from L2;
+// that is what makes b = N (the full LMMSE, NEXT-2) run on the tensor cores.
+std::vector<Window> split_for_tensor_tiles(const std::vector<Window> &geo) {
+  constexpr int32_t KEPT_MAX = 124;   // 2 * 124 + 6 (worst row alignment) <= 256
+  std::vector<Window> out;
+  for (const Window &g : geo)
+    for (int32_t o = g.o; o < g.o_next; o += KEPT_MAX) out.push_back(Window{g.a, o, std::min(g.o_next, o + KEPT_MAX)});
+  return out;
+}
+
 }  // namespace ce
 
 using ce::set_last_error;
@@ -48,12 +60,14 @@ struct ce_handle {
   double2 *d_r = nullptr;       // [n_sets][b] first column of R_hh (only d < b is needed)
   double *d_sigma2 = nullptr;   // [n_sets]
   ce::Window *d_geo = nullptr;  // [n_win]
+  std::vector<ce::Window> geo_tc;   // tensor-core window table (wide windows split into sub-windows)
+  ce::Window *d_geo_tc = nullptr;   // [geo_tc.size()]
   double2 *d_ws = nullptr;      // [n_sets][b(b+1)/2] packed Cholesky factor (FP64)
   float2 *d_W = nullptr;        // [n_sets][b][b]
   float2 *d_Wt = nullptr;       // [n_sets][b][b] transposed
   float *d_bank = nullptr;      // K3 filter bank: hi plane then lo plane, [n_sets][nkc][NR][32] each
   size_t bank_plane = 0;        // floats per plane
-  bool tf32_ok = false;         // every window fits the tensor-core tile (N <= 256)
+  bool tf32_ok = false;         // the tensor-core filter banks fit (any b; wide windows are split)
   uint16_t *d_bank16 = nullptr; // K4 filter bank: bf16 hi plane then lo plane
   size_t bank16_plane = 0;      // elements per plane
   int32_t last_kernel = -1;     // kernel launched by the most recent ce_estimate
@@ -104,6 +118,7 @@ void release(ce_handle *h) {
   cudaFree(h->d_r);
   cudaFree(h->d_sigma2);
   cudaFree(h->d_geo);
+  cudaFree(h->d_geo_tc);
   cudaFree(h->d_ws);
   cudaFree(h->d_W);
   cudaFree(h->d_Wt);
@@ -219,19 +234,23 @@ int ce_init(const ce_params *p, ce_handle **out) {
     for (int32_t d = 0; d < b; ++d)
       r_b[size_t(s) * b + d] = make_double2(p->r_hh[(size_t(s) * N + d) * 2], p->r_hh[(size_t(s) * N + d) * 2 + 1]);
   const size_t packed = size_t(b) * (b + 1) / 2;
-  h->tf32_ok = ce::tf32x3_supported(b, geo);
-  if (h->tf32_ok) {
+  h->geo_tc = ce::split_for_tensor_tiles(geo);
+  {
     int32_t nkc, NR;
     ce::tf32x3_bank_shape(b, &nkc, &NR);
     h->bank_plane = size_t(S) * nkc * NR * 32;
     ce::bf16x3_bank_shape(b, &nkc, &NR);
     h->bank16_plane = size_t(S) * nkc * NR * 32;
+    // banks: 2 fp32 planes + 2 bf16 planes; keep them well inside HBM (b = 1200: 70 MB per set)
+    const double bank_bytes = 2.0 * h->bank_plane * 4 + 2.0 * h->bank16_plane * 2;
+    h->tf32_ok = ce::tf32x3_supported(b, h->geo_tc) && bank_bytes <= 8.0e9;
   }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
   chk(cudaMalloc(&h->d_r, r_b.size() * sizeof(double2)));
   chk(cudaMalloc(&h->d_sigma2, size_t(S) * sizeof(double)));
   chk(cudaMalloc(&h->d_geo, geo.size() * sizeof(ce::Window)));
+  chk(cudaMalloc(&h->d_geo_tc, h->geo_tc.size() * sizeof(ce::Window)));
   chk(cudaMalloc(&h->d_ws, size_t(S) * packed * sizeof(double2)));
   chk(cudaMalloc(&h->d_W, size_t(S) * b * b * sizeof(float2)));
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
@@ -243,6 +262,7 @@ int ce_init(const ce_params *p, ce_handle **out) {
     chk(cudaMemcpy(h->d_r, r_b.data(), r_b.size() * sizeof(double2), cudaMemcpyHostToDevice));
     chk(cudaMemcpy(h->d_sigma2, p->sigma2, size_t(S) * sizeof(double), cudaMemcpyHostToDevice));
     chk(cudaMemcpy(h->d_geo, geo.data(), geo.size() * sizeof(ce::Window), cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(h->d_geo_tc, h->geo_tc.data(), h->geo_tc.size() * sizeof(ce::Window), cudaMemcpyHostToDevice));
   }
   if (e != cudaSuccess) {
     int st = cuda_fail(e, "ce_init: device allocation/copy");
@@ -270,7 +290,7 @@ int ce_set_kernel(ce_handle *h, int32_t kernel) {
       kernel != CE_KERNEL_BF16X3 && kernel != CE_KERNEL_BF16X3_PAIR)
     return fail(CE_EINVAL, "ce_set_kernel: unknown kernel");
   if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->tf32_ok)
-    return fail(CE_EINVAL, "ce_set_kernel: tensor-core kernels need 2*kept + row alignment <= 256 for every window");
+    return fail(CE_EINVAL, "ce_set_kernel: tensor-core filter banks do not fit for this b");
   if ((kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->even_starts)
     return fail(CE_EINVAL, "ce_set_kernel: BF16X3 / BF16X3_PAIR need every window start a_w even (16-byte TMA boxes)");
   h->kernel = kernel;
@@ -349,6 +369,11 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
   a.max_kept = h->max_kept;
   a.even_starts = h->even_starts;
   int32_t k = h->kernel;
+  if (k != CE_KERNEL_SIMT && h->tf32_ok) {   // tensor-core kernels run on the split window table
+    a.geo = h->d_geo_tc;
+    a.geo_host = h->geo_tc.data();
+    a.n_win = int32_t(h->geo_tc.size());
+  }
   if (k == CE_KERNEL_AUTO)
     k = !h->tf32_ok ? CE_KERNEL_SIMT : (ce::bf16x3_launchable(a) ? CE_KERNEL_BF16X3 : CE_KERNEL_TF32X3);
   if (k == CE_KERNEL_BF16X3 && !ce::bf16x3_launchable(a))

@@ -43,7 +43,14 @@ def _estimator(N, b, s, r, s2, kernel):
 def _run(N, b, s, r, s2, y, x, soi=None, kernel=None):
     est = _estimator(N, b, s, r, s2, kernel)
     soi_t = None if soi is None else torch.from_numpy(np.ascontiguousarray(soi, np.int32)).cuda()
-    h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), set_of_instance=soi_t)
+    ce = _ce()
+    try:
+        h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), set_of_instance=soi_t)
+    except ce.CEError as e:
+        est.close()
+        if e.status == ce.CE_EINVAL and kernel == ce.CE_KERNEL_BF16X3_PAIR:
+            pytest.skip("K5 not launchable here (resident half bank + 3 stages do not fit in shared memory)")
+        raise
     torch.cuda.synchronize()
     out = h.cpu().numpy()
     est.close()
@@ -58,7 +65,7 @@ def _inputs(cfg, m_hi=None):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 6])
 def test_config_parity_full(cfg_id, kernel):
     cfg = CONFIGS[cfg_id]
     r, s2, x, y, soi = _inputs(cfg)
@@ -140,6 +147,18 @@ def test_edge_shapes(N, b, s, M, K, T, kernel):
     if b == N:
         full = oracle.full_lmmse(y, x, r, s2, None)
         assert np.all(oracle.rel_fro_error_per_instance(h, full) <= TOL)
+
+
+def test_full_band_equals_full_lmmse():
+    """NEXT-2: b = N (config 6) is the full N x N LMMSE of Eq. 12-15; the tensor-core path splits its single
+    1200-output window into 124-output sub-windows over the same input range."""
+    ce = _ce()
+    cfg = CONFIGS[6]
+    r, s2, x, y, soi = _inputs(cfg, m_hi=16)
+    for kernel in (ce.CE_KERNEL_BF16X3, ce.CE_KERNEL_TF32X3, ce.CE_KERNEL_SIMT):
+        h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
+        ref = oracle.full_lmmse(y, x, r, s2, soi)
+        assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL), kernel
 
 
 def test_filters_match_oracle():

@@ -63,6 +63,10 @@ CONFIGS = {
               snr_range_db=(0.0, 25.0), per_slot_stats=True),
     5: Config(5, "scale_out", M=256, K=24, N=3276, Nfft=4096, slots=20, pilots_per_slot=1,
               b=126, stride=126, n_taps=24, tau_rms_s=0.5e-6, fs_hz=122.88e6, snr_db=20.0),
+    # NEXT-2: the full-band LMMSE the paper calls infeasible on its CPU,
+    # b = N on config 3's statistics -- one 1200 x 1200 filter, tensor-bound.
+    6: Config(6, "full_band", M=128, K=12, N=1200, Nfft=2048, slots=1, pilots_per_slot=1,
+              b=1200, stride=1200, n_taps=16, tau_rms_s=1e-6, fs_hz=30.72e6, snr_db=15.0),
 }
 
 
