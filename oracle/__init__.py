@@ -33,3 +33,11 @@ from .comb import (  # noqa: F401
     rect_filter,
     zoh_fill,
 )
+from .stats import (  # noqa: F401,E402
+    correlation_estimate,
+    estimate_stats,
+    ls_rows,
+    mismatched_block_mse,
+    noise_bins,
+    noise_variance_estimate,
+)
