@@ -443,6 +443,51 @@ def run_comb(args):
         dist.destroy_process_group()
 
 
+def run_stats(args):
+    """--stats: the NEXT-3 statistics estimator (K7) on the configured workload (1 GPU line)."""
+    import torch
+
+    import paper_1802_05427_b200 as ce
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    cfg = workload.get_config(args.config)
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x)
+    soi = torch.from_numpy(workload.set_of_instance(cfg)).cuda()
+    D, B = cfg.b, 32          # 32 noise-window bins: sigma2_hat from C x 32 samples (rel. s.e. < 1% on config 3)
+    nbuf = max(2, int(np.ceil(1.25 * L2_BYTES / y.nbytes)) + 1)
+    y_dev = [torch.from_numpy(y).cuda() for _ in range(nbuf)]
+    x_dev = torch.from_numpy(x).cuda()
+    for i in range(args.warmup):
+        ce.ce_stats_estimate(y_dev[i % nbuf], x_dev, D, B, soi, cfg.n_sets)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            ce.ce_stats_estimate(y_dev[i % nbuf], x_dev, D, B, soi, cfg.n_sets)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    samples = cfg.T * cfg.M * cfg.K * cfg.N
+    cols = cfg.T * cfg.M * cfg.K
+    flops = 8.0 * cols * (sum(cfg.N - d for d in range(D)) + cfg.N * B)
+    props = torch.cuda.get_device_properties(0)
+    fp32_peak = props.multi_processor_count * 128 * 2 * 1965e6
+    line = {"metric": "LS samples/s through the statistics estimator (NEXT-3)", "value": samples / (ms * 1e-3),
+            "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded workload generator)",
+            "config": _cfg_json(cfg, {"D": D, "B": B, "l2": f"rotating {nbuf} y buffers (> L2)"}),
+            "roofline": {"bound": "alu", "achieved": flops / (ms * 1e-3) / 1e12, "peak": fp32_peak / 1e12,
+                         "unit": "TFLOP/s", "frac": flops / (ms * 1e-3) / fp32_peak, "traffic": None,
+                         "kernel": "k7_accumulate", "algorithmic_flops_per_launch": flops},
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "device": props.name}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -455,6 +500,7 @@ def main():
     ap.add_argument("--ref-antennas", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stats", action="store_true", help="time the NEXT-3 statistics estimator instead")
     ap.add_argument("--comb", default=None, help="run the comb-pilot 3W/12W path on workload.COMB_CONFIGS[NAME]")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -463,6 +509,9 @@ def main():
         if args.impl == "reference":
             raise SystemExit("--impl reference times the block path's oracle; use it without --comb")
         run_comb(args)
+        return
+    if args.stats:
+        run_stats(args)
         return
     cfg = workload.get_config(args.config)
     if args.impl == "reference":

@@ -196,6 +196,27 @@ int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out);
 /* Free; NULL allowed. */
 int ce_comb_free(ce_comb_handle *h);
 
+/* ---------------------------------------------------------------------------------------------------
+ * NEXT-3: the statistics the filter build needs, estimated from the received pilots (the paper designs W
+ * from an assumed L and SNR_fixed, and fixes sigma^2 "for the lack of SNR estimation module",
+ * PAPER.md:519).  Per statistic set s, from the LS estimates H_LS = y / x (Eq. 9) of every column
+ * c = (t, m, k) of the set's instances (readings D1-D3 in DESIGN.md):
+ *   r_hat[d]   = sum_c sum_{n<N-d} H_LS[c,n+d] conj(H_LS[c,n]) / (C_s (N-d)) - sigma2_hat delta[d],  d < D
+ *   sigma2_hat = mean over c and over the B delay bins centred on N/2 of |IDFT_N(H_LS[c])|^2 (unitary)
+ * The results can be handed (via the host) to ce_init as r_hh (entries d >= D may be zero when D >= b:
+ * the filters use d < b only) and sigma2.
+ * ------------------------------------------------------------------------------------------------- */
+/* Bytes of device workspace ce_stats_estimate needs: n_sets * (2 D + 2) doubles. */
+int ce_stats_workspace_bytes(int32_t n_sets, int32_t D, int64_t *out);
+/* Device pointers, asynchronous on `stream` (K7a accumulate + K7b normalise):
+ *   d_y [T][M][K][N], d_x [T][K][N] complex64 (8-byte aligned); d_set_of_instance int32 [T] or NULL (all
+ *   set 0; instances with an out-of-range set are skipped); d_r out: complex128 [n_sets][D] interleaved;
+ *   d_sigma2 out: float64 [n_sets]; d_work: ce_stats_workspace_bytes bytes.  A set with no instance gets
+ *   NaN.  CE_EINVAL for NULL / misaligned pointers, sizes < 1, D or B > N, N > 12800. */
+int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, int32_t K, int32_t N,
+                      const int32_t *d_set_of_instance, int32_t n_sets, int32_t D, int32_t B, void *d_r,
+                      void *d_sigma2, void *d_work, void *stream);
+
 /* Static description of a status code; never NULL. */
 const char *ce_status_string(int status);
 

@@ -35,6 +35,7 @@ from .ce import (  # noqa: F401
     ce_launch_count,
     ce_selected_kernel,
     ce_set_kernel,
+    ce_stats_estimate,
     ce_status_string,
     ce_version,
     ce_window_table,

@@ -30,7 +30,7 @@ EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "c
             "ce_selected_kernel",
             "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
             "ce_version", "ce_comb_init", "ce_comb_build_filters", "ce_comb_estimate", "ce_comb_get_filters",
-            "ce_comb_launch_count", "ce_comb_free")
+            "ce_comb_launch_count", "ce_comb_free", "ce_stats_workspace_bytes", "ce_stats_estimate")
 CE_COMB_FULL, CE_COMB_SUB = 0, 1
 
 
@@ -51,6 +51,9 @@ lib.ce_comb_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32
 lib.ce_comb_get_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_comb_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
 lib.ce_comb_free.argtypes = [c_void_p]
+lib.ce_stats_workspace_bytes.argtypes = [c_int32, c_int32, POINTER(c_int64)]
+lib.ce_stats_estimate.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int32,
+                                  c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
 lib.ce_build_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]
 lib.ce_estimate_host.argtypes = lib.ce_estimate.argtypes
@@ -322,6 +325,32 @@ class CombEstimator:
             self.close()
         except Exception:
             pass
+
+
+def ce_stats_estimate(y, x, D: int, B: int, set_of_instance=None, n_sets: int = 1, stream=None):
+    """NEXT-3 statistics from device tensors y [T][M][K][N], x [T][K][N] (complex64, CUDA).
+
+    Returns (r_hat complex128 CUDA tensor [n_sets][D], sigma2_hat float64 CUDA tensor [n_sets])."""
+    import torch
+    if y.dtype != torch.complex64 or x.dtype != torch.complex64 or not (y.is_cuda and x.is_cuda):
+        raise TypeError("y and x must be complex64 CUDA tensors")
+    T, M, K, N = y.shape
+    if tuple(x.shape) != (T, K, N) or not (y.is_contiguous() and x.is_contiguous()):
+        raise ValueError("shape mismatch or non-contiguous input")
+    soi = 0
+    if set_of_instance is not None:
+        if set_of_instance.dtype != torch.int32 or not set_of_instance.is_cuda:
+            raise TypeError("set_of_instance must be a CUDA int32 tensor")
+        soi = set_of_instance.data_ptr()
+    nb = c_int64()
+    _check(lib.ce_stats_workspace_bytes(n_sets, D, ctypes.byref(nb)), "ce_stats_workspace_bytes")
+    work = torch.empty(nb.value // 8, dtype=torch.float64, device=y.device)
+    r = torch.empty((n_sets, D), dtype=torch.complex128, device=y.device)
+    s2 = torch.empty((n_sets,), dtype=torch.float64, device=y.device)
+    _check(lib.ce_stats_estimate(c_void_p(y.data_ptr()), c_void_p(x.data_ptr()), T, M, K, N, c_void_p(soi or None),
+                                 n_sets, D, B, c_void_p(r.data_ptr()), c_void_p(s2.data_ptr()),
+                                 c_void_p(work.data_ptr()), c_void_p(_stream_ptr(stream))), "ce_stats_estimate")
+    return r, s2
 
 
 def _host_ptr(a) -> int:

@@ -1,0 +1,67 @@
+"""GPU parity of the NEXT-3 statistics estimator (K7) against the oracle, and the estimate -> build ->
+estimate loop it enables."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from workload import CONFIGS
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_stats(y, x, D, B, soi=None, n_sets=1):
+    import paper_1802_05427_b200 as ce
+    soi_t = None if soi is None else torch.from_numpy(np.ascontiguousarray(soi, np.int32)).cuda()
+    r, s2 = ce.ce_stats_estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), D, B, soi_t, n_sets)
+    torch.cuda.synchronize()
+    return r.cpu().numpy(), s2.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg_id,m_hi", [(3, 64), (2, None), (4, 8), (5, 4)])
+def test_stats_parity(cfg_id, m_hi):
+    cfg = CONFIGS[cfg_id]
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x, m_hi=m_hi)
+    soi = workload.set_of_instance(cfg)
+    D, B = cfg.b, cfg.N // 8
+    r_g, s2_g = _gpu_stats(y, x, D, B, soi, cfg.n_sets)
+    for s in range(cfg.n_sets):
+        sel = soi == s
+        r_o, s2_o = oracle.estimate_stats(y[sel], x[sel], D, B)
+        assert abs(s2_g[s] / s2_o - 1) < 1e-4, (s, s2_g[s], s2_o)
+        assert np.max(np.abs(r_g[s] - r_o)) < 1e-4 * abs(r_o[0]), (s, np.max(np.abs(r_g[s] - r_o)))
+
+
+def test_stats_skipped_and_empty_sets():
+    cfg = CONFIGS[2]
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x)
+    r_g, s2_g = _gpu_stats(y, x, 10, 16, np.array([0, 7], np.int32), 3)     # instance 1: out of range
+    r_o, s2_o = oracle.estimate_stats(y[:1], x[:1], 10, 16)
+    assert abs(s2_g[0] / s2_o - 1) < 1e-4
+    assert np.isnan(s2_g[1]) and np.isnan(r_g[2]).all()                     # sets with no instance
+
+
+def test_estimated_statistics_drive_the_filters():
+    """Data-driven design: K7 statistics -> ce_init/ce_build_filters -> K4 estimate.  The MSE vs the true
+    channel is close to the matched closed form (the paper's fixed design is not needed)."""
+    import paper_1802_05427_b200 as ce
+    cfg = dataclasses.replace(CONFIGS[3], M=64)
+    x = workload.gen_pilots(cfg, 0)
+    y, H = workload.gen_instances(cfg, 0, x=x, return_channel=True)
+    r_true, s2_true = workload.channel_stats(cfg, 0)
+    r_g, s2_g = _gpu_stats(y, x, cfg.b, cfg.N // 8)
+    r_full = np.zeros((1, cfg.N), np.complex128)
+    r_full[0, :cfg.b] = r_g[0]
+    r_full[0, 0] = r_full[0, 0].real                                         # ce_init wants r[0] real
+    est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r_full, s2_g).build()
+    h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    est.close()
+    mse = np.mean(np.abs(h.cpu().numpy() - H) ** 2)
+    cf = oracle.block_mse(r_true[0], s2_true[0], cfg.b)
+    assert mse < 1.10 * cf, (mse, cf)
