@@ -334,11 +334,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
             float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
             float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
             if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
-#ifdef K4_EXP_NOSTORE
-            if (c0 < 0) hrow[ci] = a0;
-#else
             if (c0 < p.cols) hrow[ci] = a0;
-#endif
             if (c0 + 8 < p.cols) hrow[row8 + ci] = a1;
             if (c0 + 16 < p.cols) hrow[2 * row8 + ci] = a2;
             if (c0 + 24 < p.cols) hrow[3 * row8 + ci] = a3;
@@ -366,9 +362,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
-#ifdef K4_EXP_BONCE
-          if (it >= S_AB) { mbar_arrive(&b_full[s]); continue; }
-#endif
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
           const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * rows) * 32;   // bf16 elements
