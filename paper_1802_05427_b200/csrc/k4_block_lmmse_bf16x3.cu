@@ -78,7 +78,7 @@ constexpr int MAXW_PARAM = 32;             // windows carried in the kernel para
 // reads of B halve).
 template <int CG>
 struct K4Cfg {
-  static constexpr int S_AB = CG == 1 ? 3 : 4;                   // A/B stages
+  static constexpr int S_AB = CG == 1 ? 3 : 4;                   // A/B stages (measured: 4 y + 3 A/B beats 5+2, 6+2)
   static constexpr int B_PLANE = (NMAXW / CG) * 64;              // 16 KB / 8 KB
   static constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;     // 48 KB / 32 KB
   static constexpr int SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
@@ -501,8 +501,10 @@ cudaError_t dev_info(DevInfo **out) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k4_bf16x3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<1>::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k4_bf16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<2>::SMEM);
-    if (e != cudaSuccess) return e;
+    // the experimental pair mode is only available when its layout fits next to this build's stage counts
+    const bool pair_ok =
+        cudaFuncSetAttribute(k4_bf16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<2>::SMEM) == cudaSuccess;
+    if (!pair_ok) cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(d.num_sms / 2 * 2));
     cfg.blockDim = dim3(K4_THREADS);
@@ -515,7 +517,7 @@ cudaError_t dev_info(DevInfo **out) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k4_bf16x3<2>, &cfg) != cudaSuccess) {
+    if (!pair_ok || cudaOccupancyMaxActiveClusters(&n, k4_bf16x3<2>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
