@@ -248,6 +248,30 @@ def run_ours(args, cfg):
         dist.barrier()
     launches = est.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
+    graph = None
+    if args.graph_steps > 0:
+        # the same step loop replayed from a CUDA graph (launch overhead off the host; PDL edges kept)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                for i in range(args.graph_steps):
+                    ce.ce_estimate(est.handle, y_dev[i % nbuf].data_ptr(), x_dev.data_ptr(), h_dev[i % nbuf].data_ptr(),
+                                   T, M, K, soi_dev.data_ptr(), cap.cuda_stream)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        g0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        graph = {"ms_per_step": g0.elapsed_time(g1) / (reps * args.graph_steps), "steps_per_graph": args.graph_steps,
+                 "replays": reps}
+        del g
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -339,6 +363,7 @@ def run_ours(args, cfg):
                     "h2d_bytes_per_step": int(y.nbytes + x.nbytes + soi.nbytes),
                     "d2h_bytes_per_step": int(y.nbytes), "steps": e2e_steps},
             "gpu_launches": int(launches),
+            "cuda_graph": graph,
             "clocks": clk.summary(),
             "filter_build_ms": build_ms,
             "device": props.name,
@@ -392,6 +417,30 @@ def run_comb(args):
         torch.cuda.synchronize()
     launches = est.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
+    graph = None
+    if args.graph_steps > 0:
+        # the same step loop replayed from a CUDA graph (launch overhead off the host; PDL edges kept)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                for i in range(args.graph_steps):
+                    ce.ce_estimate(est.handle, y_dev[i % nbuf].data_ptr(), x_dev.data_ptr(), h_dev[i % nbuf].data_ptr(),
+                                   T, M, K, soi_dev.data_ptr(), cap.cuda_stream)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        g0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        graph = {"ms_per_step": g0.elapsed_time(g1) / (reps * args.graph_steps), "steps_per_graph": args.graph_steps,
+                 "replays": reps}
+        del g
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -497,6 +546,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 simt, 2 tf32x3, 3 bf16x3, 4 bf16x3_pair")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--graph-steps", type=int, default=100, help="steps per CUDA-graph replay (0: skip)")
     ap.add_argument("--ref-antennas", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

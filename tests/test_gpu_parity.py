@@ -308,3 +308,14 @@ def test_k4_cta_pair_mode(cfg_id, monkeypatch):
     h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=3)
     ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
     assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_antenna_permutation_equivariance(kernel):
+    """permuting antennas permutes the estimates, bit for bit (no cross-column arithmetic)."""
+    cfg = CONFIGS[3]
+    r, s2, x, y, soi = _inputs(cfg, m_hi=24)
+    perm = np.random.default_rng(5).permutation(y.shape[1])
+    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
+    hp = _run(cfg.N, cfg.b, cfg.stride, r, s2, np.ascontiguousarray(y[:, perm]), x, soi, kernel=kernel)
+    assert np.array_equal(hp.view(np.float32), h[:, perm].view(np.float32))
