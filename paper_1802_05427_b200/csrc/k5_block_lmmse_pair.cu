@@ -382,7 +382,9 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&a_full[s], ph);
+          if (it < 24) K5TR(152 + it);
           mbar_wait(&b_full[kc], bph);
+          if (it < 24) K5TR(176 + it);
           mbar_wait_cluster(&peer_ready[s], ph);
           tc_fence_after();
           if (it < 24) K5TR(104 + it);

@@ -87,7 +87,7 @@ int main(int argc, char **argv) {
   names[2] = "setup done";
   names[3] = "epi warp done";
   names[4] = "all done";
-  for (int slot = 2; slot < 152; ++slot) {
+  for (int slot = 2; slot < 200; ++slot) {
     std::vector<double> v;
     for (int c = 0; c < nsm; ++c) {
       const unsigned long long *t = &tr[size_t(c) * 256];
@@ -105,7 +105,9 @@ int main(int argc, char **argv) {
       else if (slot >= 104 && slot < 128) snprintf(buf, 64, "MMA issue it=%d", slot - 104);
       else if (slot >= 128 && slot < 136) snprintf(buf, 64, "tile MMAs committed lt=%d", slot - 128);
       else if (slot >= 136 && slot < 144) snprintf(buf, 64, "epi start lt=%d", slot - 136);
-      else snprintf(buf, 64, "epi done lt=%d", slot - 144);
+      else if (slot < 152) snprintf(buf, 64, "epi done lt=%d", slot - 144);
+      else if (slot < 176) snprintf(buf, 64, "K5 a_full passed it=%d", slot - 152);
+      else snprintf(buf, 64, "K5 b_full passed it=%d", slot - 176);
       nm = buf;
     }
     printf("%-28s median %8.0f  min %8.0f  max %8.0f ns  (n=%zu)\n", nm, v[v.size() / 2], v.front(), v.back(), v.size());

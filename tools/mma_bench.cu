@@ -1,0 +1,87 @@
+// tcgen05 kind::f16 MMA throughput microbenchmark: back-to-back 128 x N x 16 BF16 MMAs from shared-memory
+// operands with SWIZZLE_64B (64-byte K-major rows, as K4) or SWIZZLE_128B descriptors.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1802_05427_b200/csrc -o tools/mma_bench tools/mma_bench.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "tc_ptx.cuh"
+
+using namespace ce;
+
+__device__ __forceinline__ uint64_t sw128(uint32_t saddr) { return sw128_desc(saddr); }
+
+template <int SW>
+__global__ void bench(int iters, int N, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t *smem = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 256);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t d = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    // A: 128 rows, B: N rows; SW64: rows of 64 B; SW128: rows of 128 B
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32 * 1024);
+    const uint64_t ad = SW == 64 ? sw64_desc(a0) : sw128(a0);
+    const uint64_t bd = SW == 64 ? sw64_desc(b0) : sw128(b0);
+    const int ksteps = SW == 64 ? 2 : 4;            // 16-element K steps per swizzle row
+    unsigned long long t0 = clock64();
+    int ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t adv = uint64_t(2 * ks);
+        mma_bf16(d, ad + adv, bd + adv, idesc, (it | ks) != 0);
+      }
+      if ((it & 15) == 15) {
+        mma_commit(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, ph);
+    unsigned long long t1 = clock64();
+    out[blockIdx.x] = (t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(d, 256);
+  }
+}
+
+int main() {
+  unsigned long long *dout, h[148];
+  cudaMalloc(&dout, 148 * 8);
+  cudaFuncSetAttribute(bench<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int N : {256, 208, 128}) {
+    for (int grid : {1, 148}) {
+      const int iters = 4096;
+      bench<64><<<grid, 128, 100 * 1024>>>(iters, N, dout);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, dout, 8 * grid, cudaMemcpyDeviceToHost);
+      double c64 = double(h[0]) / (iters * 2);
+      bench<128><<<grid, 128, 100 * 1024>>>(iters, N, dout);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, dout, 8 * grid, cudaMemcpyDeviceToHost);
+      double c128 = double(h[0]) / (iters * 4);
+      const double flop = 2.0 * 128 * N * 16;
+      printf("N=%3d grid %3d: SW64 %.1f cyc/MMA (%.0f flop/clk)  SW128 %.1f cyc/MMA (%.0f flop/clk)  %s\n", N, grid, c64,
+             flop / c64, c128, flop / c128, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
