@@ -417,30 +417,6 @@ def run_comb(args):
         torch.cuda.synchronize()
     launches = est.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
-    graph = None
-    if args.graph_steps > 0:
-        # the same step loop replayed from a CUDA graph (launch overhead off the host; PDL edges kept)
-        g = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
-            with torch.cuda.graph(g, stream=cap):
-                for i in range(args.graph_steps):
-                    ce.ce_estimate(est.handle, y_dev[i % nbuf].data_ptr(), x_dev.data_ptr(), h_dev[i % nbuf].data_ptr(),
-                                   T, M, K, soi_dev.data_ptr(), cap.cuda_stream)
-        torch.cuda.synchronize()
-        g.replay()
-        torch.cuda.synchronize()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 5
-        g0.record(stream)
-        for _ in range(reps):
-            g.replay()
-        g1.record(stream)
-        torch.cuda.synchronize()
-        graph = {"ms_per_step": g0.elapsed_time(g1) / (reps * args.graph_steps), "steps_per_graph": args.graph_steps,
-                 "replays": reps}
-        del g
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
