@@ -8,11 +8,8 @@
 // the same complex -> real embedding as K3 (A = interleaved LS row, D = interleaved output row,
 // B_r^T rows 2i / 2i+1 = (Re W_ij, -Im W_ij) / (Im W_ij, Re W_ij)).
 //
-// Work unit: a tile = (instance t, window w, 128-column block ct).  CG = 1: one CTA per tile, M = 128.
-// CG = 2 (CE_K4_CG=2, experimental): a CTA pair runs cta_group::2 MMAs with M = 256 over two column
-// blocks; each CTA stages only half of the filter operand.  Measured slower than CG = 1 on configs 3
-// and 5 (the per-chunk peer -> leader handshake lengthens every stage's turnaround), so CG = 1 is the
-// default.
+// Work unit: a tile = (instance t, window w, 128-column block ct); one CTA per SM walks its tiles.
+// (The CTA-pair variant, cta_group::2 with the filter bank resident, is K5.)
 //
 // Pipeline (persistent, one CTA per SM, 480 threads):
 //   warp 12   : raw producer -- 2D TMA of the raw y box [128 rows x 16 complex] and the pilot box
@@ -73,16 +70,11 @@ constexpr int EPI_BYTES = 0;               // epilogue stores straight from TMEM
 constexpr int BAR_BYTES = 256;
 constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
 
-// CG = CTAs per MMA: 1 (cta_group::1, M = 128) or 2 (CTA pair, cta_group::2, M = 256: each CTA stages its
-// own 128 A rows and HALF of the filter operand's N rows, so per-SM filter traffic and tensor-core smem
-// reads of B halve).
-template <int CG>
-struct K4Cfg {
-  static constexpr int S_AB = CG == 1 ? 3 : 4;                   // A/B stages (measured: 4 y + 3 A/B beats 5+2, 6+2)
-  static constexpr int B_PLANE = (NMAXW / CG) * 64;              // 16 KB / 8 KB
-  static constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;     // 48 KB / 32 KB
-  static constexpr int SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
-};
+constexpr int S_AB = 3;                    // A/B stages (measured: 4 y + 3 A/B beats 5 + 2, 6 + 2)
+constexpr int B_PLANE = NMAXW * 64;        // 16 KB
+constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;      // 48 KB
+constexpr int K4_SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+static_assert(K4_SMEM <= 232448, "K4 shared memory");
 
 struct K4Params {
   float2 *h;
@@ -91,8 +83,7 @@ struct K4Params {
   const Window *geo;         // device window table (read only when n_win > MAXW_PARAM)
   const int32_t *soi;
   int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
-  int n_ctg;                 // column-block groups per (t, w): ceil(n_ct / CG)
-  int n_groups;              // T * n_win * n_ctg
+  int n_tiles;               // T * n_win * n_ct
   Window geo_s[MAXW_PARAM];
 };
 
@@ -100,14 +91,13 @@ struct Tile4 {
   int t, ct, a, o, kept, n0, off, nw;
 };
 
-__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank, int CG) {
+__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g) {
   Tile4 ti;
   // column block fastest (measured faster than window-fastest on configs 3-5)
-  const int ctg = g % p.n_ctg;
-  const int rest = g / p.n_ctg;
+  ti.ct = g % p.n_ct;
+  const int rest = g / p.n_ct;
   const int w = rest % p.n_win;
   ti.t = rest / p.n_win;
-  ti.ct = ctg * CG + rank;
   const Window gw = p.n_win <= MAXW_PARAM ? p.geo_s[w] : p.geo[w];
   ti.a = gw.a;
   ti.o = gw.o;
@@ -139,18 +129,12 @@ __device__ __forceinline__ float rcp_approx(float v) {
   return r;
 }
 
-template <int CG>
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
               const __grid_constant__ K4Params p) {
-  using Cfg = K4Cfg<CG>;
-  constexpr int S_AB = Cfg::S_AB;
-  constexpr int B_PLANE = Cfg::B_PLANE;
-  constexpr int AB_STAGE = Cfg::AB_STAGE;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
-  // visible to the compiler: LDS/STS instead of generic LD/ST); the same offsets in both CTAs of a pair,
-  // which the pair MMA (peer operands at the same smem offset) and the multicast commits rely on
+  // visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
   uint8_t *raw = smem + S_AB * AB_STAGE;                // [S_RAW][y 16 KB | x 4 KB]
@@ -158,17 +142,14 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(epi) + EPI_BYTES);
   uint64_t *raw_full = bars;                            // [S_RAW]
   uint64_t *raw_empty = bars + S_RAW;                   // [S_RAW]
-  uint64_t *a_full = bars + 2 * S_RAW;                  // [S_AB]  local transform done
-  uint64_t *b_full = a_full + S_AB;                     // [S_AB]  local filter slice landed
+  uint64_t *a_full = bars + 2 * S_RAW;                  // [S_AB]  transform done
+  uint64_t *b_full = a_full + S_AB;                     // [S_AB]  filter chunk landed
   uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
-  uint64_t *peer_ready = st_empty + S_AB;               // [S_AB]  (pair leader) peer's stage is full
-  uint64_t *tmem_full = peer_ready + S_AB;              // [2]
-  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp (x CG)
+  uint64_t *tmem_full = st_empty + S_AB;                // [2]
+  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rank = CG > 1 ? int(cluster_ctarank()) : 0;
-  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;
 #ifdef CE_K4_TRACE
   if (tid == 0 && g_k4_trace) {
     unsigned long long gt;
@@ -186,11 +167,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       mbar_init(&a_full[s], NTR);
       mbar_init(&b_full[s], 1);
       mbar_init(&st_empty[s], 1);
-      mbar_init(&peer_ready[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4 * CG);
+      mbar_init(&tmem_empty[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -198,15 +178,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
   }
-  if (warp == 13) {
-    if (CG == 1)
-      tmem_alloc(tmem_slot, 512);
-    else
-      tmem_alloc2(tmem_slot, 512);
-  }
+  if (warp == 13) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
-  if (CG > 1) cluster_sync();         // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tid == 0) {
@@ -227,8 +201,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     if (lane == 0) {
       const uint32_t xbytes = uint32_t(p.K) * CK * 8;
       int it = 0;
-      for (int g = unit; g < p.n_groups; g += n_units) {
-        const Tile4 ti = decode4(p, g, rank, CG);
+      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
+        const Tile4 ti = decode4(p, g);
         const int row0 = ti.t * p.cols + ti.ct * TM;
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_RAW;
@@ -246,8 +220,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int jp = tid & 7;            // complex pair 2jp, 2jp+1 of the 16-complex chunk
     const int rb = tid >> 3;           // rows rb + 32 i, i < 4
     int it = 0;
-    for (int g = unit; g < p.n_groups; g += n_units) {
-      const Tile4 ti = decode4(p, g, rank, CG);
+    for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
+      const Tile4 ti = decode4(p, g);
       const int c_first = ti.ct * TM + rb;
       const int x_first = c_first % p.K;
       const int x_step = 32 % p.K;
@@ -305,8 +279,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int q = warp & 3;
     const int rA = lane >> 2, cq = lane & 3;
     int lt = 0;
-    for (int g = unit; g < p.n_groups; g += n_units, ++lt) {
-      const Tile4 ti = decode4(p, g, rank, CG);
+    for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
+      const Tile4 ti = decode4(p, g);
       const bool set_ok = tile_set(p, ti.t) >= 0;
       const int acc = lt & 1;
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
@@ -342,63 +316,43 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
       }
       if (tid == 256 && lt < 8) K4TR(144 + lt);
+      __syncwarp();
       if (lane == 0) {
         tc_fence_before();
-        if (CG == 1 || rank == 0)
-          mbar_arrive(&tmem_empty[acc]);
-        else
-          mbar_arrive_remote(&tmem_empty[acc], 0);      // the pair leader's MMA waits on both CTAs
+        mbar_arrive(&tmem_empty[acc]);
       }
     }
   } else if (warp == 14) {
-    // ---------------------------------------------------------------- B producer (this CTA's N rows)
+    // ---------------------------------------------------------------- B producer
     if (lane == 0) {
       int it = 0;
-      for (int g = unit; g < p.n_groups; g += n_units) {
-        const Tile4 ti = decode4(p, g, rank, CG);
+      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
+        const Tile4 ti = decode4(p, g);
         const int set = max(tile_set(p, ti.t), 0);
-        const int rows = ti.nw / CG;                           // multiple of 8 (nw is a multiple of 16)
-        const uint32_t bytes = uint32_t(rows) * 64;            // per plane
+        const uint32_t bytes = uint32_t(ti.nw) * 64;          // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
-          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * rows) * 32;   // bf16 elements
+          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0) * 32;   // bf16 elements
           uint8_t *bh = ab + s * AB_STAGE + 2 * A_PLANE;
           bulk_g2s(bh, p.bank_hi + src, bytes, &b_full[s]);
           bulk_g2s(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s]);
         }
       }
-      // drain: the commits of the last use of every stage have arrived here, so nothing arrives on this
-      // CTA's barriers after the closing barrier
-      for (int i = 0; i < S_AB; ++i, ++it) mbar_wait(&st_empty[it % S_AB], ((it / S_AB) & 1) ^ 1);
     }
   } else {
-    // ---------------------------------------------------------------- MMA issuer / pair forwarder (warp 13)
-    if (lane == 0 && CG == 2 && rank == 1) {
-      // pair follower: tell the leader when this CTA's half of each stage is in shared memory
-      int it = 0;
-      for (int g = unit; g < p.n_groups; g += n_units)
-        for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % S_AB;
-          const uint32_t ph = (it / S_AB) & 1;
-          mbar_wait(&a_full[s], ph);
-          mbar_wait(&b_full[s], ph);
-          mbar_arrive_remote(&peer_ready[s], 0);
-        }
-    } else if (lane == 0) {
+    // ---------------------------------------------------------------- MMA issuer (warp 13)
+    if (lane == 0) {
       int it = 0, lt = 0;
-      for (int g = unit; g < p.n_groups; g += n_units, ++lt) {
-        const Tile4 ti = decode4(p, g, rank, CG);
+      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
+        const Tile4 ti = decode4(p, g);
         const int acc = lt & 1;
-        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128 * CG
+        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(ti.nw >> 3) << 17) |
-                               (uint32_t((TM * CG) >> 4) << 24);
-        if (CG == 1)
-          mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
-        else
-          mbar_wait_cluster(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+                               (uint32_t(TM >> 4) << 24);
+        mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * NMAXW);
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
@@ -406,7 +360,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const uint32_t ph = (it / S_AB) & 1;
           mbar_wait(&a_full[s], ph);
           mbar_wait(&b_full[s], ph);
-          if (CG == 2) mbar_wait_cluster(&peer_ready[s], ph);
           tc_fence_after();
           if (it < 24) K4TR(104 + it);
           uint8_t *st = ab + s * AB_STAGE;
@@ -417,25 +370,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const int nks = min(2, nks_total - 2 * kc);
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t adv = uint64_t(2 * ks);      // +32 bytes along K
-            if (CG == 1) {
-              mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-              mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
-              mma_bf16(d, al + adv, bh + adv, idesc, 1u);
-            } else {
-              mma_bf16_pair(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-              mma_bf16_pair(d, ah + adv, bl + adv, idesc, 1u);
-              mma_bf16_pair(d, al + adv, bh + adv, idesc, 1u);
-            }
+            mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+            mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
+            mma_bf16(d, al + adv, bh + adv, idesc, 1u);
           }
-          if (CG == 1)
-            mma_commit(&st_empty[s]);
-          else
-            mma_commit_pair(&st_empty[s]);
+          mma_commit(&st_empty[s]);
         }
-        if (CG == 1)
-          mma_commit(&tmem_full[acc]);
-        else
-          mma_commit_pair(&tmem_full[acc]);
+        mma_commit(&tmem_full[acc]);
         if (lt < 8) K4TR(128 + lt);
       }
     }
@@ -443,15 +384,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   tc_fence_before();
   if (tid == 256) K4TR(3);
   __syncthreads();
-  if (CG > 1) cluster_sync();
   if (tid == 0) K4TR(4);
   if (warp == 13) {
     __syncwarp();
     tc_fence_after();
-    if (CG == 1)
-      tmem_dealloc(tmem_base, 512);
-    else
-      tmem_dealloc2(tmem_base, 512);
+    tmem_dealloc(tmem_base, 512);
   }
 }
 
@@ -482,12 +419,10 @@ __global__ void k4_build_bank(const float2 *__restrict__ W, int b, int nkc, int 
   }
 }
 
-// Per-device launch facts: smem attributes set once, SM count, and how many CTA pairs can be resident
-// at once (a pair needs two free SMs of one TPC).
+// Per-device launch facts: smem attribute set once, SM count.
 struct DevInfo {
   bool init = false;
   int num_sms = 0;
-  int max_pairs = 0;
 };
 cudaError_t dev_info(DevInfo **out) {
   static DevInfo infos[64];
@@ -499,29 +434,8 @@ cudaError_t dev_info(DevInfo **out) {
   if (!d.init) {
     e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k4_bf16x3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<1>::SMEM);
+    e = cudaFuncSetAttribute(k4_bf16x3, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
     if (e != cudaSuccess) return e;
-    // the experimental pair mode is only available when its layout fits next to this build's stage counts
-    const bool pair_ok =
-        cudaFuncSetAttribute(k4_bf16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4Cfg<2>::SMEM) == cudaSuccess;
-    if (!pair_ok) cudaGetLastError();
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(d.num_sms / 2 * 2));
-    cfg.blockDim = dim3(K4_THREADS);
-    cfg.dynamicSmemBytes = K4Cfg<2>::SMEM;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (!pair_ok || cudaOccupancyMaxActiveClusters(&n, k4_bf16x3<2>, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      n = 0;
-    }
-    d.max_pairs = n;
     d.init = true;
   }
   *out = &d;
@@ -581,45 +495,28 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   p.cols = a.M * a.K;
   p.n_ct = (p.cols + TM - 1) / TM;
   for (int w = 0; w < MAXW_PARAM; ++w) p.geo_s[w] = w < a.n_win && a.geo_host ? a.geo_host[w] : Window{0, 0, 0};
-  // CTA pairs when the column blocks pair up exactly and pairs can cover (nearly) every SM; CE_K4_CG=1|2
-  // overrides (experiments and tests)
-  const char *env = std::getenv("CE_K4_CG");
-  const int want = env ? std::atoi(env) : 0;
-  int CG = 1;   // measured: the pair's per-chunk cross-CTA handshake costs more than the halved B traffic saves
-  if (want == 1) CG = 1;
-  if (want == 2 && di->max_pairs > 0) CG = 2;
-  p.n_ctg = (p.n_ct + CG - 1) / CG;
-  const long long groups = (long long)a.T * a.n_win * p.n_ctg;
-  if (groups > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  p.n_groups = int(groups);
+  const long long tiles = (long long)a.T * a.n_win * p.n_ct;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  p.n_tiles = int(tiles);
   CUtensorMap tmy, tmx;
   if (!cached_map(&tmy, a.y, a.N, (long long)a.T * p.cols, TM) ||
       !cached_map(&tmx, a.x, a.N, (long long)a.T * a.K, a.K))
     return cudaErrorInvalidValue;
-  const int max_units = CG == 1 ? di->num_sms : di->max_pairs;
-  const int n_units = int(groups < max_units ? groups : max_units);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(n_units * CG));
+  cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
   cfg.blockDim = dim3(K4_THREADS);
-  cfg.dynamicSmemBytes = CG == 1 ? K4Cfg<1>::SMEM : K4Cfg<2>::SMEM;
+  cfg.dynamicSmemBytes = K4_SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   int na = 0;
 #ifndef K4_NO_PDL
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
 #endif
-  if (CG > 1) {
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = unsigned(CG);
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  e = CG == 1 ? cudaLaunchKernelEx(&cfg, k4_bf16x3<1>, tmy, tmx, p) : cudaLaunchKernelEx(&cfg, k4_bf16x3<2>, tmy, tmx, p);
+  e = cudaLaunchKernelEx(&cfg, k4_bf16x3, tmy, tmx, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

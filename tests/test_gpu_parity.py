@@ -298,18 +298,6 @@ def test_kernels_agree_and_auto():
     est.close()
 
 
-@pytest.mark.parametrize("cfg_id", [3, 1])
-def test_k4_cta_pair_mode(cfg_id, monkeypatch):
-    """K4's experimental CTA-pair mode (cta_group::2, CE_K4_CG=2) meets the same bar; config 1 has a single
-    column block, so the pair's second CTA runs a dummy block whose stores are all masked."""
-    monkeypatch.setenv("CE_K4_CG", "2")
-    cfg = CONFIGS[cfg_id]
-    r, s2, x, y, soi = _inputs(cfg)
-    h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=3)
-    ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
-    assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL)
-
-
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_antenna_permutation_equivariance(kernel):
     """permuting antennas permutes the estimates, bit for bit (no cross-column arithmetic)."""
