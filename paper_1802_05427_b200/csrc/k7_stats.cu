@@ -9,9 +9,10 @@
 //   r_hat[d]   = R_hat[d] - sigma2_hat delta[d]
 // The noise window is the B delay bins centred on N/2, far from the channel's delay support (reading D2).
 //
-// K7a: one CTA per column: LS row and the N twiddles exp(j 2 pi n / N) in shared memory; threads split the
-// D lags (x as many n-ranges as fit in 256 threads) and then the B noise bins; per-CTA partial sums are
-// added in FP64 to per-set accumulators.  K7b: one thread per set normalises.
+// K7a: one CTA per K7_CPB columns of one instance: the N twiddles exp(j 2 pi n / N) and, column by column, the LS
+// row in shared memory; threads own blocks of 4 lags (x as many n-ranges as fit in 256 threads, partial sums
+// carried in registers across the columns) and then (bin, n-range) pairs of the noise window; one FP64
+// reduction + atomics per CTA into the per-set accumulators.  K7b: one thread per set normalises.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -24,76 +25,140 @@ namespace {
 
 constexpr int K7_THREADS = 256;
 
+constexpr int K7_CPB = 1;      // columns per CTA, same instance (measured on config 3: 1 -> 139 us, 2 -> 143, 8 -> 184)
+constexpr int LB = 4;          // lags per thread
+
 __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                             int M, int K, int N, const int32_t *__restrict__ soi,
                                                             int n_sets, int D, int B, double *__restrict__ acc) {
   extern __shared__ float2 sm7[];
   float2 *ls = sm7;                                  // [N]
   float2 *tw = sm7 + N;                              // [N] exp(+j 2 pi n / N)
-  __shared__ double part[2 * K7_THREADS];
-  const int col = blockIdx.x;                        // (t * M + m) * K + k
-  const int t = col / (M * K), k = col % K;
+  __shared__ double part[2 * LB * K7_THREADS];       // [lag in block][thread][re, im]
+  const int MK = M * K;
+  const int n_cb = (MK + K7_CPB - 1) / K7_CPB;
+  const int t = blockIdx.x / n_cb, c_lo = (blockIdx.x % n_cb) * K7_CPB, c_hi = min(MK, c_lo + K7_CPB);
   const int set = soi ? soi[t] : 0;
   if (set < 0 || set >= n_sets) return;              // out-of-range set: the instance is skipped
-  const float2 *yr = y + size_t(col) * N;
-  const float2 *xr = x + (size_t(t) * K + k) * N;
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const float2 yv = yr[n], xv = xr[n];
-    const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
-    ls[n] = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
-    double sv, cv;
-    sincospi(2.0 * n / N, &sv, &cv);
-    tw[n] = make_float2(float(cv), float(sv));
+    // FP32 twiddle (|error| < 2^-23); the exact reduction 2n/N in [0, 2) keeps the argument small
+    float sv, cv;
+    sincospif(2.0f * float(n) / float(N), &sv, &cv);
+    tw[n] = make_float2(cv, sv);
+  }
+  double *acc_s = acc + size_t(set) * (2 * D + 2);   // [re, im] x D lags, noise power, column count
+  // lag work split: thread -> (block of LB consecutive lags, n-range); partial sums stay in registers
+  // across the CTA's columns and are reduced once at the end
+  const int n_lb = (D + LB - 1) / LB;
+  const int nparts = max(1, int(blockDim.x) / n_lb);
+  const int lanes = blockDim.x / nparts;
+  const int lb = int(threadIdx.x) % lanes, pr = int(threadIdx.x) / lanes;
+  const bool lag_thread = lb < n_lb && pr < nparts && lanes >= n_lb;
+  float re[LB] = {0.f, 0.f, 0.f, 0.f}, im[LB] = {0.f, 0.f, 0.f, 0.f};
+  // noise work split: thread -> (bin, n-range)
+  const int lo = N / 2 - B / 2;
+  const int bparts = max(1, int(blockDim.x) / min(B, int(blockDim.x)));
+  const int bins_per_pass = blockDim.x / bparts;
+  double pw = 0;
+  for (int c = c_lo; c < c_hi; ++c) {
+    const float2 *yr = y + (size_t(t) * MK + c) * N;
+    const float2 *xr = x + (size_t(t) * K + c % K) * N;
+    __syncthreads();                                 // previous column's ls fully consumed
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const float2 yv = yr[n], xv = xr[n];
+      const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
+      ls[n] = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
+    }
+    __syncthreads();
+    // lags: ls[n] is shared by LB lags and ls[n+d..n+d+LB-1] slides (8 FMA per shared-memory read)
+    for (int l0 = 0; l0 < n_lb; l0 += lanes) {
+      const int lbk = l0 + lb;
+      if (lanes >= n_lb ? lag_thread : (lbk < n_lb && pr < nparts)) {
+        const int d = lbk * LB;
+        const int len = N - d, chunk = (len + nparts - 1) / nparts;
+        const int n0 = pr * chunk, n1 = min(len, n0 + chunk);
+        float2 win[LB];
+#pragma unroll
+        for (int i = 0; i < LB; ++i) win[i] = (n0 + d + i < N) ? ls[n0 + d + i] : make_float2(0.f, 0.f);
+        float r4[LB] = {0.f, 0.f, 0.f, 0.f}, i4[LB] = {0.f, 0.f, 0.f, 0.f};
+        for (int n = n0; n < n1; ++n) {
+          const float2 bv = ls[n];
+#pragma unroll
+          for (int i = 0; i < LB; ++i) {             // win[i] = ls[n + d + i] (zero beyond N)
+            r4[i] = fmaf(win[i].x, bv.x, fmaf(win[i].y, bv.y, r4[i]));
+            i4[i] = fmaf(win[i].y, bv.x, fmaf(-win[i].x, bv.y, i4[i]));
+          }
+#pragma unroll
+          for (int i = 0; i < LB - 1; ++i) win[i] = win[i + 1];
+          win[LB - 1] = (n + d + LB < N) ? ls[n + d + LB] : make_float2(0.f, 0.f);
+        }
+        if (lanes >= n_lb) {
+#pragma unroll
+          for (int i = 0; i < LB; ++i) {
+            re[i] += r4[i];
+            im[i] += i4[i];
+          }
+        } else {                                     // D > 4 * 256: no register carry, add directly
+          for (int i = 0; i < LB && d + i < D; ++i) {
+            atomicAdd(&acc_s[2 * (d + i)], double(r4[i]));
+            atomicAdd(&acc_s[2 * (d + i) + 1], double(i4[i]));
+          }
+        }
+      }
+    }
+    // noise window: the complex partial sums of a bin are combined before taking |.|^2
+    for (int b0 = 0; b0 < B; b0 += bins_per_pass) {
+      const int bi = b0 + int(threadIdx.x) % bins_per_pass, bp = int(threadIdx.x) / bins_per_pass;
+      float nre = 0.f, nim = 0.f;
+      if (bi < B && bp < bparts) {
+        const int kap = lo + bi;
+        const int chunk = (N + bparts - 1) / bparts;
+        const int n0 = bp * chunk, n1 = min(N, n0 + chunk);
+        int idx = int((static_cast<long long>(n0) * kap) % N);   // (n * kap) mod N
+        for (int n = n0; n < n1; ++n) {
+          const float2 w = tw[idx], v = ls[n];
+          nre = fmaf(v.x, w.x, fmaf(-v.y, w.y, nre));
+          nim = fmaf(v.x, w.y, fmaf(v.y, w.x, nim));
+          idx += kap;
+          if (idx >= N) idx -= N;
+        }
+      }
+      __syncthreads();                               // part[] free
+      part[2 * threadIdx.x] = nre;
+      part[2 * threadIdx.x + 1] = nim;
+      __syncthreads();
+      if (threadIdx.x < bins_per_pass && b0 + int(threadIdx.x) < B) {
+        double sr = 0, si = 0;
+        for (int q = 0; q < bparts; ++q) {
+          sr += part[2 * (q * bins_per_pass + threadIdx.x)];
+          si += part[2 * (q * bins_per_pass + threadIdx.x) + 1];
+        }
+        pw += sr * sr + si * si;
+      }
+    }
+  }
+  // one reduction and one set of atomics per CTA
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < LB; ++i) {
+    part[2 * (i * K7_THREADS + threadIdx.x)] = re[i];
+    part[2 * (i * K7_THREADS + threadIdx.x) + 1] = im[i];
   }
   __syncthreads();
-  double *acc_s = acc + size_t(set) * (2 * D + 2);   // [re, im] x D lags, noise power, column count
-  // lags: thread -> (d, n-range)
-  const int nparts = max(1, int(blockDim.x) / D);
-  for (int d0 = 0; d0 < D; d0 += blockDim.x / nparts) {
-    const int d = d0 + int(threadIdx.x) % (blockDim.x / nparts), pr = int(threadIdx.x) / (blockDim.x / nparts);
-    float re = 0.f, im = 0.f;
-    if (d < D && pr < nparts) {
-      const int len = N - d, chunk = (len + nparts - 1) / nparts;
-      const int n1 = min(len, (pr + 1) * chunk);
-      for (int n = pr * chunk; n < n1; ++n) {
-        const float2 a = ls[n + d], b = ls[n];     // a conj(b)
-        re = fmaf(a.x, b.x, fmaf(a.y, b.y, re));
-        im = fmaf(a.y, b.x, fmaf(-a.x, b.y, im));
+  if (lanes >= n_lb && threadIdx.x < n_lb) {
+    for (int i = 0; i < LB; ++i) {
+      const int dd = int(threadIdx.x) * LB + i;
+      if (dd >= D) break;
+      double sr = 0, si = 0;
+      for (int q = 0; q < nparts; ++q) {
+        sr += part[2 * (i * K7_THREADS + q * lanes + threadIdx.x)];
+        si += part[2 * (i * K7_THREADS + q * lanes + threadIdx.x) + 1];
       }
+      atomicAdd(&acc_s[2 * dd], sr);
+      atomicAdd(&acc_s[2 * dd + 1], si);
     }
-    part[2 * threadIdx.x] = re;
-    part[2 * threadIdx.x + 1] = im;
-    __syncthreads();
-    if (threadIdx.x < blockDim.x / nparts) {
-      const int dd = d0 + threadIdx.x;
-      if (dd < D) {
-        double sr = 0, si = 0;
-        for (int q = 0; q < nparts; ++q) {
-          sr += part[2 * (q * (blockDim.x / nparts) + threadIdx.x)];
-          si += part[2 * (q * (blockDim.x / nparts) + threadIdx.x) + 1];
-        }
-        atomicAdd(&acc_s[2 * dd], sr);
-        atomicAdd(&acc_s[2 * dd + 1], si);
-      }
-    }
-    __syncthreads();
   }
-  // noise window: B delay bins centred on N/2
-  const int lo = N / 2 - B / 2;
-  double pw = 0;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    const int kap = lo + i;
-    float re = 0.f, im = 0.f;
-    int idx = 0;                                      // (n * kap) mod N
-    for (int n = 0; n < N; ++n) {
-      const float2 w = tw[idx], v = ls[n];
-      re = fmaf(v.x, w.x, fmaf(-v.y, w.y, re));
-      im = fmaf(v.x, w.y, fmaf(v.y, w.x, im));
-      idx += kap;
-      if (idx >= N) idx -= N;
-    }
-    pw += double(re) * re + double(im) * im;
-  }
+  __syncthreads();
   part[threadIdx.x] = pw;
   __syncthreads();
   for (int st = blockDim.x / 2; st > 0; st >>= 1) {
@@ -102,7 +167,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
   }
   if (threadIdx.x == 0) {
     atomicAdd(&acc_s[2 * D], part[0] / N);            // unitary IDFT: |sum|^2 / N
-    atomicAdd(&acc_s[2 * D + 1], 1.0);
+    atomicAdd(&acc_s[2 * D + 1], double(c_hi - c_lo));
   }
 }
 
@@ -151,7 +216,8 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   if ((reinterpret_cast<uintptr_t>(d_r) | reinterpret_cast<uintptr_t>(d_sigma2) | reinterpret_cast<uintptr_t>(d_work)) & 7u)
     return fail(CE_EINVAL, "ce_stats_estimate: outputs / workspace must be 8-byte aligned");
   const long long cols = (long long)T * M * K;
-  if (cols > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
+  const long long ctas = (long long)T * ((static_cast<long long>(M) * K + ce::K7_CPB - 1) / ce::K7_CPB);
+  if (cols > 0x7fffffffLL || ctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
   const size_t smem = size_t(2) * N * sizeof(float2);
   if (smem > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large (N <= 12800)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -163,7 +229,7 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
     return CE_ECUDA;
   }
-  ce::k7_accumulate<<<unsigned(cols), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
+  ce::k7_accumulate<<<unsigned(ctas), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
                                                                   static_cast<const float2 *>(d_x), M, K, N,
                                                                   d_set_of_instance, n_sets, D, B, acc);
   ce::k7_finalize<<<(n_sets + 127) / 128, 128, 0, st>>>(acc, n_sets, N, D, B, static_cast<double *>(d_r),
