@@ -347,6 +347,26 @@ def run_ours(args, cfg):
                "sample": f"{runs} runs of oracle LS+block apply (complex128) on antennas [0,{m}) of config "
                          f"{cfg.cfg_id} instance 0, {el:.1f} s"}
 
+    # multi-GPU verification (outside the timed region): NCCL all-gather of the antenna shards, and rank 0
+    # recomputes the whole global batch on its own GPU -- the sharded result must match it bit for bit
+    # (SURVEY.md §8(e) shard invariance)
+    verify = None
+    if world > 1 and not args.no_verify:
+        try:
+            from paper_1802_05427_b200.shard import gather_antenna_shards
+            full = gather_antenna_shards(h_dev[(args.steps - 1) % nbuf], world * cfg.M)
+            if rank == 0:
+                y_all = workload.gen_instances(cfg, 0, m_lo=0, m_hi=world * cfg.M, x=x)
+                h_ref = est.estimate(torch.from_numpy(y_all).to(dev), x_dev, set_of_instance=soi_dev)
+                torch.cuda.synchronize()
+                verify = {"nccl_all_gather_bytes": int(full.numel() * 8),
+                          "bitwise_equal_to_single_gpu": bool(torch.equal(torch.view_as_real(full),
+                                                                          torch.view_as_real(h_ref)))}
+            del full
+        except Exception as exc:       # never let the check take the measurement down
+            verify = {"error": repr(exc)[:200]}
+        dist.barrier()
+
     if rank == 0:
         line = {
             "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value, "unit": "estimates/s",
@@ -364,6 +384,7 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": int(y.nbytes), "steps": e2e_steps},
             "gpu_launches": int(launches),
             "cuda_graph": graph,
+            "multi_gpu_verify": verify,
             "clocks": clk.summary(),
             "filter_build_ms": build_ms,
             "device": props.name,
@@ -526,6 +547,7 @@ def main():
     ap.add_argument("--ref-antennas", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip the N>1 NCCL gather + single-GPU bitwise check")
     ap.add_argument("--stats", action="store_true", help="time the NEXT-3 statistics estimator instead")
     ap.add_argument("--comb", default=None, help="run the comb-pilot 3W/12W path on workload.COMB_CONFIGS[NAME]")
     args = ap.parse_args()
