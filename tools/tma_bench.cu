@@ -265,16 +265,18 @@ int main(int argc, char **argv) {
       if (size_t(stages) * sb > 220 * 1024) continue;
       // ~1.6 GB read per run
       const int use_rb = nrb;
-      stream<<<nsm, 32, stages * sb>>>(tm, br, bf, use_rb, ncb, stages, sb, sink);
+      const int grid = getenv("TMA_GRID") ? atoi(getenv("TMA_GRID")) : nsm;
+      const int use_rb2 = grid < nsm ? (use_rb * grid) / nsm + 1 : use_rb;
+      stream<<<grid, 32, stages * sb>>>(tm, br, bf, use_rb2, ncb, stages, sb, sink);
       cudaEventRecord(e0);
-      stream<<<nsm, 32, stages * sb>>>(tm, br, bf, use_rb, ncb, stages, sb, sink);
+      stream<<<grid, 32, stages * sb>>>(tm, br, bf, use_rb2, ncb, stages, sb, sink);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
-      const double moved = double(use_rb) * ncb * sb;
-      printf("box %3d rows x %4d B  stages %2d (%3d KB)  %7.1f GB/s  (%.2f GB/s/SM)  %s\n", br, bf * 4, stages,
-             stages * sb / 1024, moved / ms / 1e6, moved / ms / 1e6 / nsm, cudaGetErrorString(cudaGetLastError()));
+      const double moved = double(use_rb2) * ncb * sb;
+      printf("grid %3d box %3d rows x %4d B  stages %2d (%3d KB)  %7.1f GB/s  (%.2f GB/s/SM)  %s\n", grid, br, bf * 4,
+             stages, stages * sb / 1024, moved / ms / 1e6, moved / ms / 1e6 / grid, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
