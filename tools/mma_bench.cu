@@ -62,6 +62,50 @@ __global__ void bench(int iters, int N, unsigned long long *out) {
   }
 }
 
+// CTA pair: cta_group::2, M = 256 (128 rows per CTA), N columns with N/2 B rows staged in each CTA.
+__global__ void __cluster_dims__(2, 1, 1) bench_pair(int iters, int N, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t *smem = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc2(&slot, 256);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t d = slot;
+  if (threadIdx.x == 0 && cluster_ctarank() == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+    const uint64_t ad = sw64_desc(smem_u32(smem)), bd = sw64_desc(smem_u32(smem + 32 * 1024));
+    unsigned long long t0 = clock64();
+    int ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int ks = 0; ks < 2; ++ks) mma_bf16_pair(d, ad + uint64_t(2 * ks), bd + uint64_t(2 * ks), idesc, (it | ks) != 0);
+      if ((it & 15) == 15) {
+        mma_commit_pair(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    mma_commit_pair(&bar);
+    mbar_wait(&bar, ph);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc2(d, 256);
+  }
+}
+
 int main() {
   unsigned long long *dout, h[148];
   cudaMalloc(&dout, 148 * 8);
@@ -82,6 +126,16 @@ int main() {
       printf("N=%3d grid %3d: SW64 %.1f cyc/MMA (%.0f flop/clk)  SW128 %.1f cyc/MMA (%.0f flop/clk)  %s\n", N, grid, c64,
              flop / c64, c128, flop / c128, cudaGetErrorString(cudaGetLastError()));
     }
+  }
+  cudaFuncSetAttribute(bench_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int N : {256, 208}) {
+    const int iters = 4096;
+    bench_pair<<<2, 128, 100 * 1024>>>(iters, N, dout);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, dout, 8, cudaMemcpyDeviceToHost);
+    const double c = double(h[0]) / (iters * 2);
+    printf("PAIR M=256 N=%3d: %.1f cyc/MMA (%.0f flop/clk per SM)  %s\n", N, c, 2.0 * 128 * N * 16 / c,
+           cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
