@@ -34,15 +34,22 @@ bool window_table(int32_t N, int32_t b, int32_t s, std::vector<Window> *out) {
   return true;
 }
 
-// Tensor-core tiles hold at most 256 accumulator columns (2 * kept + row alignment <= 256): windows that
-// keep more outputs are split into output sub-windows over the same LS input range (same a_w, b), each
-// keeping <= 124 consecutive outputs.  Reading the full b-wide input per sub-window re-reads y from L2;
-// that is what makes b = N (the full LMMSE, NEXT-2) run on the tensor cores.
+// Tensor-core tiles hold at most 256 accumulator columns: a piece [o, o + len) of a window starting at a
+// occupies MMA N = off + 2 len (rounded up to 16), off = 2 (o - a) mod 8 being the 8-row alignment of the
+// filter-bank rows, so it fits iff off + 2 len <= 256.  Windows that fit stay whole (config 5: 126 outputs,
+// off = 0); wider ones are split into the fewest output sub-windows over the same LS input range (same a_w,
+// b), each as long as its alignment allows (125-128 outputs).  Reading the full b-wide input per
+// sub-window re-reads y from L2; that is what makes b = N (the full LMMSE, NEXT-2) run on the tensor cores.
 std::vector<Window> split_for_tensor_tiles(const std::vector<Window> &geo) {
-  constexpr int32_t KEPT_MAX = 124;   // 2 * 124 + 6 (worst row alignment) <= 256
+  constexpr int32_t NMAX = 256;
   std::vector<Window> out;
   for (const Window &g : geo)
-    for (int32_t o = g.o; o < g.o_next; o += KEPT_MAX) out.push_back(Window{g.a, o, std::min(g.o_next, o + KEPT_MAX)});
+    for (int32_t o = g.o; o < g.o_next;) {
+      const int32_t off = (2 * (o - g.a)) & 7;
+      const int32_t len = std::min(g.o_next - o, (NMAX - off) / 2);
+      out.push_back(Window{g.a, o, o + len});
+      o += len;
+    }
   return out;
 }
 

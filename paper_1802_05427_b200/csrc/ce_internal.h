@@ -20,7 +20,7 @@ struct Window {
 
 // Host-side window table; returns false for invalid sizes.
 bool window_table(int32_t N, int32_t b, int32_t s, std::vector<Window> *out);
-// The same windows with every window keeping > 124 outputs split into output sub-windows (tensor-core tiles).
+// The same windows with every window too wide for one 256-column MMA tile split into output sub-windows.
 std::vector<Window> split_for_tensor_tiles(const std::vector<Window> &geo);
 
 // Arguments of one contraction launch (K2 / K3).

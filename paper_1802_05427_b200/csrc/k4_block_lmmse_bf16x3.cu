@@ -40,11 +40,14 @@ namespace ce {
 namespace {
 
 // Optional per-CTA event trace (tools/k4_trace.cu builds with -DCE_K4_TRACE; the product build has none).
+// Timing ablations (results wrong by construction; tools/k4_trace.sh <tag> -D...): K4_ABL_NOSTORE,
+// K4_ABL_NOMMA, K4_ABL_NOTRANSFORM, K4_ABL_NOB (no filter-chunk copies).
 #ifdef CE_K4_TRACE
 __device__ unsigned long long *g_k4_trace;
-#define K4TR(slot)                                                             \
-  do {                                                                         \
-    if (g_k4_trace) g_k4_trace[size_t(blockIdx.x) * 256 + (slot)] = clock64(); \
+#define K4TR(slot)                                                                \
+  do {                                                                            \
+    const unsigned long long c_ = clock64(); /* read before the pointer load */  \
+    if (g_k4_trace) g_k4_trace[size_t(blockIdx.x) * 256 + (slot)] = c_;           \
   } while (0)
 #else
 #define K4TR(slot) \
@@ -123,6 +126,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_addr, float hi_addr) {
 }
 __device__ __forceinline__ float bf16_lo_f(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi_f(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+// output store; K4_ST_CS: streaming (evict-first) cache hint
+__device__ __forceinline__ void st_out(float2 *ptr, float2 v) {
+#ifdef K4_ST_CS
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(ptr), "f"(v.x), "f"(v.y) : "memory");
+#else
+  *ptr = v;
+#endif
+}
 __device__ __forceinline__ float rcp_approx(float v) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -173,12 +184,16 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       mbar_init(&tmem_empty[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    K4TR(203);
   }
   if (warp == 12 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
   }
-  if (warp == 13) tmem_alloc(tmem_slot, 512);
+  if (warp == 13) {
+    tmem_alloc(tmem_slot, 512);
+    if (lane == 0) K4TR(202);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -194,6 +209,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #ifndef K4_NO_PDL
   if (!(warp == 14 && p.soi == nullptr)) pdl_wait();
 #endif
+  if (tid == 12 * 32) K4TR(200);
   const int nks_total = (2 * p.b + 15) / 16;   // 16-element (bf16) MMA K steps over 2b
 
   if (warp == 12) {
@@ -203,6 +219,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       int it = 0;
       for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
         const Tile4 ti = decode4(p, g);
+        if (g == int(blockIdx.x)) K4TR(201);
         const int row0 = ti.t * p.cols + ti.ct * TM;
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_RAW;
@@ -229,6 +246,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         const int sr = it % S_RAW, sa = it % S_AB;
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
         if (tid == 0 && it < 24) K4TR(32 + it);
+#ifdef K4_ABL_NOTRANSFORM
+        mbar_arrive(&raw_empty[sr]);
+        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
+        mbar_arrive(&a_full[sa]);
+        continue;
+#endif
         const float4 *ry = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE);
         const float4 *rx = reinterpret_cast<const float4 *>(raw + sr * RAW_STAGE + RAWY);
         float4 yv[4], xv[4];
@@ -308,10 +331,14 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
             float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
             float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
             if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
-            if (c0 < p.cols) hrow[ci] = a0;
-            if (c0 + 8 < p.cols) hrow[row8 + ci] = a1;
-            if (c0 + 16 < p.cols) hrow[2 * row8 + ci] = a2;
-            if (c0 + 24 < p.cols) hrow[3 * row8 + ci] = a3;
+#ifdef K4_ABL_NOSTORE
+            if (a0.x == 123.f && a3.y == 77.f) hrow[ci] = a1;   // keeps the TMEM loads live; ~never stores
+#else
+            if (c0 < p.cols) st_out(hrow + ci, a0);
+            if (c0 + 8 < p.cols) st_out(hrow + row8 + ci, a1);
+            if (c0 + 16 < p.cols) st_out(hrow + 2 * row8 + ci, a2);
+            if (c0 + 24 < p.cols) st_out(hrow + 3 * row8 + ci, a3);
+#endif
           }
         }
       }
@@ -333,6 +360,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
+#ifdef K4_ABL_NOB
+          mbar_arrive(&b_full[s]);
+          continue;
+#endif
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
           const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0) * 32;   // bf16 elements
@@ -370,14 +401,17 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const int nks = min(2, nks_total - 2 * kc);
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t adv = uint64_t(2 * ks);      // +32 bytes along K
+#ifndef K4_ABL_NOMMA
             mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
             mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
             mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+#endif
           }
           mma_commit(&st_empty[s]);
         }
         mma_commit(&tmem_full[acc]);
         if (lt < 8) K4TR(128 + lt);
+        else if (lt < 32) K4TR(152 + lt - 8);
       }
     }
   }
@@ -385,6 +419,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (tid == 256) K4TR(3);
   __syncthreads();
   if (tid == 0) K4TR(4);
+#ifdef CE_K4_TRACE
+  if (tid == 0 && g_k4_trace) {   // end globaltimer: tools/k4_trace.cu calibrates clock64 against it
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_k4_trace[size_t(blockIdx.x) * 256 + 5] = gt;
+  }
+#endif
   if (warp == 13) {
     __syncwarp();
     tc_fence_after();

@@ -82,12 +82,25 @@ int main(int argc, char **argv) {
   for (int c = 0; c < nsm; ++c)
     if (tr[size_t(c) * 256]) { g0 = std::min(g0, tr[size_t(c) * 256]); g1 = std::max(g1, tr[size_t(c) * 256]); ++used; }
   printf("CTAs %d, start skew (globaltimer) %llu ns\n", used, g1 - g0);
-  const double ghz = 1.965;
+  // effective SM clock: clock64 ticks over globaltimer ns, start (slots 1/0) to end (slots 4/5)
+  std::vector<double> rates;
+  for (int c = 0; c < nsm; ++c) {
+    const unsigned long long *t = &tr[size_t(c) * 256];
+    if (t[0] && t[5] && t[5] > t[0]) rates.push_back(double(t[4] - t[1]) / double(t[5] - t[0]));
+  }
+  std::sort(rates.begin(), rates.end());
+  const double ghz = rates.empty() ? 1.965 : rates[rates.size() / 2];
+  printf("effective clock %.3f GHz (median over CTAs; %zu CTAs)\n", ghz, rates.size());
   const char *names[256] = {};
   names[2] = "setup done";
   names[3] = "epi warp done";
   names[4] = "all done";
-  for (int slot = 2; slot < 200; ++slot) {
+  names[200] = "producer after pdl_wait";
+  names[201] = "producer first decode";
+  names[202] = "tmem alloc done";
+  names[203] = "barrier init done";
+  for (int slot = 2; slot < 204; ++slot) {
+    if (slot == 5) continue;   // end globaltimer
     std::vector<double> v;
     for (int c = 0; c < nsm; ++c) {
       const unsigned long long *t = &tr[size_t(c) * 256];
@@ -106,7 +119,7 @@ int main(int argc, char **argv) {
       else if (slot >= 128 && slot < 136) snprintf(buf, 64, "tile MMAs committed lt=%d", slot - 128);
       else if (slot >= 136 && slot < 144) snprintf(buf, 64, "epi start lt=%d", slot - 136);
       else if (slot < 152) snprintf(buf, 64, "epi done lt=%d", slot - 144);
-      else if (slot < 176) snprintf(buf, 64, "K5 a_full passed it=%d", slot - 152);
+      else if (slot < 176) snprintf(buf, 64, "K5 a_full passed it=%d / K4 tile commit lt=%d", slot - 152, slot - 144);
       else snprintf(buf, 64, "K5 b_full passed it=%d", slot - 176);
       nm = buf;
     }
