@@ -61,22 +61,26 @@ constexpr int CK = 16;                     // complex per K chunk = 32 bf16 = 64
 constexpr int TM = 128;                    // A rows (columns c) per CTA
 constexpr int NMAXW = 256;                 // MMA N max (2*kept + row alignment)
 constexpr int KMAX = 32;                   // pilot rows per raw stage (K <= 32)
-#ifndef K4_S_RAW
-#define K4_S_RAW 4
-#endif
-constexpr int S_RAW = K4_S_RAW;            // raw y/x stages
+constexpr int S_RAW_MAX = 4;               // raw y/x stages: 4, or 3 when the TMA-store staging is in use
 constexpr int A_PLANE = TM * 64;           // 8 KB
 constexpr int RAWY = TM * CK * 8;          // 16 KB
 constexpr int RAWX = KMAX * CK * 8;        // 4 KB
 constexpr int RAW_STAGE = RAWY + RAWX;     // 20 KB
-constexpr int EPI_BYTES = 0;               // epilogue stores straight from TMEM registers
+constexpr int EPI_WARP = 4096;             // TMA-store staging per epilogue warp: [32 rows][128 B], SWIZZLE_128B
+constexpr int EPI_BYTES = 4 * EPI_WARP;
 constexpr int BAR_BYTES = 256;
 constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
 
-constexpr int S_AB = 3;                    // A/B stages (measured: 4 y + 3 A/B beats 5 + 2, 6 + 2)
+#ifndef K4_S_AB
+#define K4_S_AB 3
+#endif
+constexpr int S_AB = K4_S_AB;              // A/B stages (measured: 4 y + 3 A/B beats 5 + 2, 6 + 2)
 constexpr int B_PLANE = NMAXW * 64;        // 16 KB
 constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;      // 48 KB
-constexpr int K4_SMEM = S_AB * AB_STAGE + S_RAW * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+// with staging: 3 A/B + 3 raw stages + staging; without: 3 A/B + 4 raw stages
+constexpr int K4_SMEM_ST = S_AB * AB_STAGE + (S_RAW_MAX - 1) * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+constexpr int K4_SMEM_NOST = S_AB * AB_STAGE + S_RAW_MAX * RAW_STAGE + BAR_BYTES + 1024;
+constexpr int K4_SMEM = K4_SMEM_ST > K4_SMEM_NOST ? K4_SMEM_ST : K4_SMEM_NOST;
 static_assert(K4_SMEM <= 232448, "K4 shared memory");
 
 struct K4Params {
@@ -87,6 +91,8 @@ struct K4Params {
   const int32_t *soi;
   int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
   int n_tiles;               // T * n_win * n_ct
+  int tma_store;             // 1: interior 32-float column blocks leave through SW128 staging + TMA stores
+  int s_raw;                 // raw ring depth (3 with staging, 4 without)
   Window geo_s[MAXW_PARAM];
 };
 
@@ -142,18 +148,19 @@ __device__ __forceinline__ float rcp_approx(float v) {
 
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
-              const __grid_constant__ K4Params p) {
+              const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K4Params p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
   // visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
+  const int S_RAW = p.s_raw;
   uint8_t *raw = smem + S_AB * AB_STAGE;                // [S_RAW][y 16 KB | x 4 KB]
-  float *epi = reinterpret_cast<float *>(raw + S_RAW * RAW_STAGE);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(epi) + EPI_BYTES);
-  uint64_t *raw_full = bars;                            // [S_RAW]
-  uint64_t *raw_empty = bars + S_RAW;                   // [S_RAW]
-  uint64_t *a_full = bars + 2 * S_RAW;                  // [S_AB]  transform done
+  uint8_t *epi = raw + S_RAW * RAW_STAGE;               // [4 warps][EPI_WARP] when p.tma_store
+  uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? EPI_BYTES : 0));
+  uint64_t *raw_full = bars;                            // [S_RAW_MAX]
+  uint64_t *raw_empty = bars + S_RAW_MAX;               // [S_RAW_MAX]
+  uint64_t *a_full = bars + 2 * S_RAW_MAX;              // [S_AB]  transform done
   uint64_t *b_full = a_full + S_AB;                     // [S_AB]  filter chunk landed
   uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
   uint64_t *tmem_full = st_empty + S_AB;                // [2]
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #endif
   if (tid == 0) {
     K4TR(1);
-    for (int s = 0; s < S_RAW; ++s) {
+    for (int s = 0; s < S_RAW_MAX; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], NTR);
     }
@@ -321,6 +328,33 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         tmem_ld16x256b_x4(ta, v0);                       // lanes q*32 + 0..15
         tmem_ld16x256b_x4(ta + (16u << 16), v1);         // lanes q*32 + 16..31
         tmem_ld_wait();
+        // Interior 32-float column blocks (inside the kept range, 16-byte aligned in global memory, all
+        // 32 rows of this warp inside the instance) leave through SW128 staging and one TMA store of
+        // [32 rows][128 B]: full-line writes issued by the TMA engine.  The rest use direct stores.
+        if (p.tma_store && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
+            ti.ct * TM + q * 32 + 32 <= p.cols) {
+          uint8_t *stg = epi + q * EPI_WARP;
+          if (lane == 0) bulk_wait_read0();              // the previous store has read the staging buffer
+          __syncwarp();
+          const uint32_t nanb = 0x7fc00000u;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int chunk = 2 * m + (cq >> 1), half = (cq & 1) * 8;
+            const int rr[4] = {rA, rA + 8, rA + 16, rA + 24};
+            const uint32_t *src[4] = {&v0[4 * m], &v0[4 * m + 2], &v1[4 * m], &v1[4 * m + 2]};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint2 *>(stg + rr[j] * 128 + ((chunk ^ (rr[j] & 7)) << 4) + half) =
+                  set_ok ? make_uint2(src[j][0], src[j][1]) : make_uint2(nanb, nanb);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32);
+            bulk_commit();
+          }
+          continue;
+        }
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int f = cb * 32 + 8 * m + 2 * cq - ti.off;   // output float index within the kept range
@@ -349,6 +383,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         mbar_arrive(&tmem_empty[acc]);
       }
     }
+    if (p.tma_store && lane == 0) bulk_wait0();          // every TMA store of this warp has completed
   } else if (warp == 14) {
     // ---------------------------------------------------------------- B producer
     if (lane == 0) {
@@ -539,14 +574,21 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   const long long tiles = (long long)a.T * a.n_win * p.n_ct;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   p.n_tiles = int(tiles);
-  CUtensorMap tmy, tmx;
+  CUtensorMap tmy, tmx, tmh = {};
   if (!cached_map(&tmy, a.y, a.N, (long long)a.T * p.cols, TM) ||
       !cached_map(&tmx, a.x, a.N, (long long)a.T * a.K, a.K))
     return cudaErrorInvalidValue;
+  // TMA stores pay off when CTAs walk several tiles (their stores overlap the next tiles' loads; measured
+  // -11% on config 5); a one-tile-per-SM launch (config 3) keeps the 4-deep raw ring and direct stores.
+  static const int env_st = getenv("CE_K4_TMA_STORE") ? atoi(getenv("CE_K4_TMA_STORE")) : -1;   // experiments
+  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) &&
+                (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0;
+  if (p.tma_store && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true)) return cudaErrorInvalidValue;
+  p.s_raw = p.tma_store ? S_RAW_MAX - 1 : S_RAW_MAX;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
   cfg.blockDim = dim3(K4_THREADS);
-  cfg.dynamicSmemBytes = K4_SMEM;
+  cfg.dynamicSmemBytes = p.tma_store ? K4_SMEM_ST : K4_SMEM_NOST;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   int na = 0;
@@ -557,7 +599,7 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
 #endif
   cfg.attrs = at;
   cfg.numAttrs = na;
-  e = cudaLaunchKernelEx(&cfg, k4_bf16x3, tmy, tmx, p);
+  e = cudaLaunchKernelEx(&cfg, k4_bf16x3, tmy, tmx, tmh, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

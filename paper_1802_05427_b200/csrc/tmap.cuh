@@ -37,26 +37,41 @@ bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_ro
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [rows][2N] float tensor, box [box_rows][box_floats], SWIZZLE_128B (box_floats * 4 == 128): store maps.
+bool make_map_sw128(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(2) * N * 4};
+  cuuint32_t box[2] = {cuuint32_t(32), cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Tensor maps are a pure function of (pointer, N, rows, box rows): cache the last few per host thread so
 // back-to-back calls on the same buffers skip the driver encode.
 struct MapCacheEntry {
   const void *ptr;
   int N, box_rows;
   long long rows;
+  bool sw128;
   CUtensorMap map;
 };
-bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
-  constexpr int NC = 16;
+bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows, bool sw128 = false) {
+  constexpr int NC = 24;
   static thread_local MapCacheEntry cache[NC];
   static thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i)
-    if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows) {
+    if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows &&
+        cache[i].sw128 == sw128) {
       *m = cache[i].map;
       return true;
     }
-  if (!make_map(m, ptr, N, rows, box_rows)) return false;
+  if (!(sw128 ? make_map_sw128(m, ptr, N, rows, box_rows) : make_map(m, ptr, N, rows, box_rows))) return false;
   MapCacheEntry &e = cache[next];
-  e = MapCacheEntry{ptr, N, box_rows, rows, *m};
+  e = MapCacheEntry{ptr, N, box_rows, rows, sw128, *m};
   next = (next + 1) % NC;
   if (used < NC) ++used;
   return true;

@@ -307,3 +307,17 @@ def test_antenna_permutation_equivariance(kernel):
     h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
     hp = _run(cfg.N, cfg.b, cfg.stride, r, s2, np.ascontiguousarray(y[:, perm]), x, soi, kernel=kernel)
     assert np.array_equal(hp.view(np.float32), h[:, perm].view(np.float32))
+
+
+@pytest.mark.parametrize("tma_store", ["1", "0"])
+def test_k4_store_paths(tma_store):
+    """K4's epilogue with its TMA-store column blocks forced on (and off) for every launch, on shapes that
+    exercise both store paths and their boundaries (tests/_k4_store_paths.py, one subprocess per setting)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CE_K4_TMA_STORE=tma_store, PYTHONPATH=root)
+    res = subprocess.run([sys.executable, os.path.join(root, "tests", "_k4_store_paths.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
