@@ -92,6 +92,7 @@ struct K4Params {
   int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
   int n_tiles;               // T * n_win * n_ct
   int tma_store;             // 1: interior 32-float column blocks leave through SW128 staging + TMA stores
+  int tma_last;              // 1: the same for each CTA's last tile, staged in the then idle A/B ring
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
   Window geo_s[MAXW_PARAM];
 };
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
       const Tile4 ti = decode4(p, g);
       const bool set_ok = tile_set(p, ti.t) >= 0;
+      const bool last = p.tma_last && g + int(gridDim.x) >= p.n_tiles;
       const int acc = lt & 1;
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -331,10 +333,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         // Interior 32-float column blocks (inside the kept range, 16-byte aligned in global memory, all
         // 32 rows of this warp inside the instance) leave through SW128 staging and one TMA store of
         // [32 rows][128 B]: full-line writes issued by the TMA engine.  The rest use direct stores.
-        if (p.tma_store && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
-            ti.ct * TM + q * 32 + 32 <= p.cols) {
-          uint8_t *stg = epi + q * EPI_WARP;
-          if (lane == 0) bulk_wait_read0();              // the previous store has read the staging buffer
+        if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf &&
+            ((2 * ti.o - ti.off) & 3) == 0 && ti.ct * TM + q * 32 + 32 <= p.cols) {
+          // last tile: every MMA has completed, the A/B ring is idle -> one staging buffer per (warp, block)
+          uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + q * EPI_WARP;
+          if (!last && lane == 0) bulk_wait_read0();     // the previous store has read the staging buffer
           __syncwarp();
           const uint32_t nanb = 0x7fc00000u;
 #pragma unroll
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         mbar_arrive(&tmem_empty[acc]);
       }
     }
-    if (p.tma_store && lane == 0) bulk_wait0();          // every TMA store of this warp has completed
+    if ((p.tma_store || p.tma_last) && lane == 0) bulk_wait0();   // every TMA store of this warp completed
   } else if (warp == 14) {
     // ---------------------------------------------------------------- B producer
     if (lane == 0) {
@@ -581,9 +584,12 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   // TMA stores pay off when CTAs walk several tiles (their stores overlap the next tiles' loads; measured
   // -11% on config 5); a one-tile-per-SM launch (config 3) keeps the 4-deep raw ring and direct stores.
   static const int env_st = getenv("CE_K4_TMA_STORE") ? atoi(getenv("CE_K4_TMA_STORE")) : -1;   // experiments
-  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) &&
-                (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0;
-  if (p.tma_store && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true)) return cudaErrorInvalidValue;
+  const bool st_ok = (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0;
+  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) && st_ok;
+  static const int env_last = getenv("CE_K4_TMA_LAST") ? atoi(getenv("CE_K4_TMA_LAST")) : 1;   // experiments
+  p.tma_last = env_last != 0 && st_ok && S_AB * AB_STAGE >= 4 * 8 * EPI_WARP;
+  if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
+    return cudaErrorInvalidValue;
   p.s_raw = p.tma_store ? S_RAW_MAX - 1 : S_RAW_MAX;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
