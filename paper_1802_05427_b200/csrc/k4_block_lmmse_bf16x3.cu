@@ -147,6 +147,72 @@ __device__ __forceinline__ float rcp_approx(float v) {
   return r;
 }
 
+// One 32-float column block cb of a finished tile: TMEM accumulator (this warp's 32 lanes) -> global.
+// Interior blocks (inside the kept range, 16-byte aligned in global memory, all 32 rows of the warp inside
+// the instance) leave through SW128 staging and one TMA store of [32 rows][128 B] (full-line writes issued
+// by the TMA engine); the rest use direct 8-byte stores (8 rows x 32 B per warp instruction).  On a CTA's
+// last tile the A/B ring is idle and every (warp, block) gets its own staging buffer there.
+__device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *tmh, uint32_t tmem_base, uint8_t *ab,
+                                          uint8_t *epi, const Tile4 &ti, int cb, int q, int lane, int acc, bool last,
+                                          bool set_ok) {
+  const int rA = lane >> 2, cq = lane & 3;
+  const int nf = 2 * ti.kept;
+  // tcgen05.ld 16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row
+  uint32_t v0[16], v1[16];
+  const uint32_t ta = tmem_base + uint32_t(acc * NMAXW + cb * 32) + (uint32_t(q * 32) << 16);
+  tmem_ld16x256b_x4(ta, v0);                         // lanes q*32 + 0..15: rows rA, rA + 8
+  tmem_ld16x256b_x4(ta + (16u << 16), v1);           // lanes q*32 + 16..31: rows rA + 16, rA + 24
+  tmem_ld_wait();
+  if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
+      ti.ct * TM + q * 32 + 32 <= p.cols) {
+    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + q * EPI_WARP;
+    if (!last && lane == 0) bulk_wait_read0();       // the previous store has read the staging buffer
+    __syncwarp();
+    const uint32_t nanb = 0x7fc00000u;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int chunk = 2 * m + (cq >> 1), half = (cq & 1) * 8;
+      const int rr[4] = {rA, rA + 8, rA + 16, rA + 24};
+      const uint32_t *src[4] = {&v0[4 * m], &v0[4 * m + 2], &v1[4 * m], &v1[4 * m + 2]};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<uint2 *>(stg + rr[j] * 128 + ((chunk ^ (rr[j] & 7)) << 4) + half) =
+            set_ok ? make_uint2(src[j][0], src[j][1]) : make_uint2(nanb, nanb);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32);
+      bulk_commit();
+    }
+    return;
+  }
+  const int c0 = ti.ct * TM + q * 32 + rA;           // rows c0, c0 + 8, c0 + 16, c0 + 24
+  float2 *hrow = p.h + (size_t(ti.t) * p.cols + c0) * p.N + ti.o;
+  const size_t row8 = size_t(8) * p.N;
+  const float qnan = __int_as_float(0x7fc00000);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int f = cb * 32 + 8 * m + 2 * cq - ti.off;   // output float index within the kept range
+    if (f >= 0 && f < nf) {
+      const int ci = f >> 1;
+      float2 a0 = make_float2(__uint_as_float(v0[4 * m]), __uint_as_float(v0[4 * m + 1]));
+      float2 a1 = make_float2(__uint_as_float(v0[4 * m + 2]), __uint_as_float(v0[4 * m + 3]));
+      float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
+      float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
+      if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
+#ifdef K4_ABL_NOSTORE
+      if (a0.x == 123.f && a3.y == 77.f) hrow[ci] = a1;   // keeps the TMEM loads live; ~never stores
+#else
+      if (c0 < p.cols) st_out(hrow + ci, a0);
+      if (c0 + 8 < p.cols) st_out(hrow + row8 + ci, a1);
+      if (c0 + 16 < p.cols) st_out(hrow + 2 * row8 + ci, a2);
+      if (c0 + 24 < p.cols) st_out(hrow + 3 * row8 + ci, a3);
+#endif
+    }
+  }
+}
+
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
               const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K4Params p) {
@@ -334,7 +400,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // TMEM -> registers (16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row)
     // -> direct 8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes.
     const int q = warp & 3;
-    const int rA = lane >> 2, cq = lane & 3;
     int lt = 0;
     for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
       const Tile4 ti = decode4(p, g);
@@ -344,67 +409,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
       tc_fence_after();
       if (tid == 256 && lt < 8) K4TR(136 + lt);
-      const int nf = 2 * ti.kept;
-      const int ncb = (ti.off + nf + 31) / 32;
-      const int c0 = ti.ct * TM + q * 32 + rA;         // rows c0, c0 + 8, c0 + 16, c0 + 24
-      float2 *hrow = p.h + (size_t(ti.t) * p.cols + c0) * p.N + ti.o;
-      const size_t row8 = size_t(8) * p.N;
-      const float qnan = __int_as_float(0x7fc00000);
-      for (int cb = 0; cb < ncb; ++cb) {
-        uint32_t v0[16], v1[16];
-        const uint32_t ta = tmem_base + uint32_t(acc * NMAXW + cb * 32) + (uint32_t(q * 32) << 16);
-        tmem_ld16x256b_x4(ta, v0);                       // lanes q*32 + 0..15
-        tmem_ld16x256b_x4(ta + (16u << 16), v1);         // lanes q*32 + 16..31
-        tmem_ld_wait();
-        // Interior 32-float column blocks (inside the kept range, 16-byte aligned in global memory, all
-        // 32 rows of this warp inside the instance) leave through SW128 staging and one TMA store of
-        // [32 rows][128 B]: full-line writes issued by the TMA engine.  The rest use direct stores.
-        if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf &&
-            ((2 * ti.o - ti.off) & 3) == 0 && ti.ct * TM + q * 32 + 32 <= p.cols) {
-          // last tile: every MMA has completed, the A/B ring is idle -> one staging buffer per (warp, block)
-          uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + q * EPI_WARP;
-          if (!last && lane == 0) bulk_wait_read0();     // the previous store has read the staging buffer
-          __syncwarp();
-          const uint32_t nanb = 0x7fc00000u;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int chunk = 2 * m + (cq >> 1), half = (cq & 1) * 8;
-            const int rr[4] = {rA, rA + 8, rA + 16, rA + 24};
-            const uint32_t *src[4] = {&v0[4 * m], &v0[4 * m + 2], &v1[4 * m], &v1[4 * m + 2]};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<uint2 *>(stg + rr[j] * 128 + ((chunk ^ (rr[j] & 7)) << 4) + half) =
-                  set_ok ? make_uint2(src[j][0], src[j][1]) : make_uint2(nanb, nanb);
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32);
-            bulk_commit();
-          }
-          continue;
-        }
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int f = cb * 32 + 8 * m + 2 * cq - ti.off;   // output float index within the kept range
-          if (f >= 0 && f < nf) {
-            const int ci = f >> 1;
-            float2 a0 = make_float2(__uint_as_float(v0[4 * m]), __uint_as_float(v0[4 * m + 1]));
-            float2 a1 = make_float2(__uint_as_float(v0[4 * m + 2]), __uint_as_float(v0[4 * m + 3]));
-            float2 a2 = make_float2(__uint_as_float(v1[4 * m]), __uint_as_float(v1[4 * m + 1]));
-            float2 a3 = make_float2(__uint_as_float(v1[4 * m + 2]), __uint_as_float(v1[4 * m + 3]));
-            if (!set_ok) a0 = a1 = a2 = a3 = make_float2(qnan, qnan);
-#ifdef K4_ABL_NOSTORE
-            if (a0.x == 123.f && a3.y == 77.f) hrow[ci] = a1;   // keeps the TMEM loads live; ~never stores
-#else
-            if (c0 < p.cols) st_out(hrow + ci, a0);
-            if (c0 + 8 < p.cols) st_out(hrow + row8 + ci, a1);
-            if (c0 + 16 < p.cols) st_out(hrow + 2 * row8 + ci, a2);
-            if (c0 + 24 < p.cols) st_out(hrow + 3 * row8 + ci, a3);
-#endif
-          }
-        }
-      }
+      const int ncb = (ti.off + 2 * ti.kept + 31) / 32;
+      for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok);
       if (tid == 256 && lt < 8) K4TR(144 + lt);
       __syncwarp();
       if (lane == 0) {
