@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU call: build, GPU tests, smoke, default bench line + reference arm, K4 sweep, ncu launch list and
+# --set full captures of k4_bf16x3 on configs 3 and 5.   Usage: tools/evidence_round.sh TAG
+TAG=${1:-r01}
+mkdir -p gpurun_out
+python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build_${TAG}.log 2>&1 || { echo BUILD FAILED; tail -20 gpurun_out/build_${TAG}.log; exit 1; }
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest gpu exit $?"; tail -2 gpurun_out/pytest_gpu_${TAG}.log
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_${TAG}.log 2>&1; echo "smoke exit $?"
+timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench exit $?"; cat gpurun_out/bench_${TAG}.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; echo "ref exit $?"
+bash tools/sweep.sh "0" "4 5 6" 200
+bash tools/sweep.sh "1 2" "3" 300
+bash tools/profile_round.sh ${TAG}
