@@ -387,8 +387,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           const int r = rb + 32 * i;
           // SW64 K-major: row r at r*64 bytes, 16-byte chunk (jp>>1) ^ ((r>>1)&3), 8-byte half (jp&1)
           const int off = r * 64 + ((((jp >> 1) ^ ((r >> 1) & 3))) << 4) + ((jp & 1) << 3);
+#ifdef K4_ABL_NOASTORE
+          if (hv[i][0] == 0x12345u && lv[i][1] == 0x777u) *reinterpret_cast<uint2 *>(ah + off) = make_uint2(hv[i][1], lv[i][0]);
+#else
           *reinterpret_cast<uint2 *>(ah + off) = make_uint2(hv[i][0], hv[i][1]);
           *reinterpret_cast<uint2 *>(al + off) = make_uint2(lv[i][0], lv[i][1]);
+#endif
         }
         fence_proxy_async();
         if (tid == 0 && it < 24) K4TR(56 + it);
