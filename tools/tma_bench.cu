@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -113,7 +114,7 @@ __global__ void copyk(const __grid_constant__ CUtensorMap tm, float *dst, long l
 // columns 2(a_w + 16 kc) of rows t*cols + ct*128.  order 0: ct fastest; 1: w fastest; 2: kc-outer
 // (all tiles of a CTA interleaved per chunk is not modelled).
 __global__ void k4pat(const __grid_constant__ CUtensorMap tm, int T, int n_win, int n_ct, int b, int s_stride,
-                      int cols, int nkc, int stages, int order, unsigned long long *sink) {
+                      int cols, int nkc, int stages, int order, unsigned long long *sink, int bw = 32) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bars[16];
   if (threadIdx.x != 0) return;
@@ -127,16 +128,17 @@ __global__ void k4pat(const __grid_constant__ CUtensorMap tm, int T, int n_win, 
     if (order == 0) { ct = tile % n_ct; w = (tile / n_ct) % n_win; t = tile / (n_ct * n_win); }
     else { w = tile % n_win; ct = (tile / n_win) % n_ct; t = tile / (n_ct * n_win); }
     const int a = min(w * s_stride, 2 * 1638 - b);   // N = 3276 for this bench tensor
-    *c0 = 2 * (a + 16 * kc);
+    *c0 = 2 * a + bw * kc;
     *c1 = t * cols + ct * 128;
   };
   auto issue = [&](int j, int s) {
     int c0, c1;
     coords(j, &c0, &c1);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[s])), "r"(16384u) : "memory");
+    const uint32_t sbytes = 128u * uint32_t(bw) * 4u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[s])), "r"(sbytes) : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(sm + size_t(s) * 16384)),
+            smem_u32(sm + size_t(s) * sbytes)),
         "l"(reinterpret_cast<uint64_t>(&tm)), "r"(c0), "r"(c1), "r"(smem_u32(&bars[s]))
         : "memory");
   };
@@ -150,7 +152,7 @@ __global__ void k4pat(const __grid_constant__ CUtensorMap tm, int T, int n_win, 
             smem_u32(&bars[s])),
         "r"((j / stages) & 1)
         : "memory");
-    acc += sm[size_t(s) * 16384 + 7];
+    acc += sm[size_t(s) * 128u * bw * 4u + 7];
     if (next < total) issue(next++, s);
   }
   sink[blockIdx.x] = acc;
@@ -202,6 +204,34 @@ int main(int argc, char **argv) {
           printf("K4PAT T=%d order %d stages %d: %.1f us  %.1f GB/s  %s\n", Tn, order, st, ms * 1e3, moved / ms / 1e6,
                  cudaGetErrorString(cudaGetLastError()));
         }
+  }
+  {
+    // K4 read pattern with wider boxes: 128 rows x {128, 256, 512} B, the same bytes in flight (~64-128 KB)
+    cudaEvent_t c0, c1;
+    cudaEventCreate(&c0);
+    cudaEventCreate(&c1);
+    for (int bw : {32, 64, 128}) {
+      CUtensorMap tm;
+      cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
+      cuuint64_t str[1] = {cuuint64_t(2) * N * 4};
+      cuuint32_t box[2] = {cuuint32_t(bw), 128}, es[2] = {1, 1};
+      enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const int nkc = (2 * 126 + bw - 1) / bw;
+      for (int kb : {64, 128, 192}) {
+        const int st = std::max(1, std::min(16, kb * 1024 / (128 * bw * 4)));
+        k4pat<<<nsm, 32, st * 128 * bw * 4>>>(tm, 20, 26, 48, 126, 126, 6144, nkc, st, 0, sink, bw);
+        cudaEventRecord(c0);
+        k4pat<<<nsm, 32, st * 128 * bw * 4>>>(tm, 20, 26, 48, 126, 126, 6144, nkc, st, 0, sink, bw);
+        cudaEventRecord(c1);
+        cudaEventSynchronize(c1);
+        float ms;
+        cudaEventElapsedTime(&ms, c0, c1);
+        const double moved = 20.0 * 26 * 48 * nkc * 128.0 * bw * 4;
+        printf("K4PAT-W box 128 x %3d B stages %2d (%3d KB): %.1f us  %.1f GB/s  %s\n", bw * 4, st, st * bw / 2, ms * 1e3,
+               moved / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
   }
   float *dcopy;
   cudaMalloc(&dcopy, bytes);
