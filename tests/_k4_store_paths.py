@@ -44,6 +44,19 @@ def main():
         ok = bool(np.all(err <= 1e-4)) and bool(np.isfinite(got).all())
         print(f"N={N} b={b} s={s} M={M} K={K} T={T}: max rel err {err.max():.2e} {'ok' if ok else 'FAIL'}")
         bad += not ok
+        if T >= 2:
+            # an out-of-range statistic set makes that instance NaN through either store path; the others exact
+            est = ce.ChannelEstimator(N, b, s, r, s2)
+            ce.ce_set_kernel(est.handle, ce.CE_KERNEL_BF16X3)
+            est.build()
+            soi = torch.tensor([0] + [7] * (T - 1), dtype=torch.int32, device="cuda")
+            hb = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda(), set_of_instance=soi)
+            torch.cuda.synchronize()
+            hb = hb.cpu().numpy()
+            est.close()
+            ok2 = bool(np.isnan(hb[1:]).all()) and bool(np.all(oracle.rel_fro_error_per_instance(hb[:1], ref[:1]) <= 1e-4))
+            print(f"  bad set index on instances 1..{T - 1}: {'ok' if ok2 else 'FAIL'}")
+            bad += not ok2
     return 1 if bad else 0
 
 
