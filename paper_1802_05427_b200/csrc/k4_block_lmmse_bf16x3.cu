@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (!(warp == 14 && p.soi == nullptr)) pdl_wait();
 #endif
 #ifdef CE_K4_TRACE
-  unsigned long long c_pdl = clock64(), c_dec = 0, c_tma0 = 0;   // producer prologue, stored at the end
+  unsigned long long c_pdl = clock64(), c_dec = 0, c_tma0 = 0, c_w0 = 0;   // producer prologue, stored at the end
 #endif
   const int nks_total = (2 * p.b + 15) / 16;   // 16-element (bf16) MMA K steps over 2b
 
@@ -314,6 +314,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         for (int kc = 0; kc < nkc0; ++kc, ++it) {
           const int s = it % S_RAW;
           mbar_wait(&raw_empty[s], ((it / S_RAW) & 1) ^ 1);
+#ifdef CE_K4_TRACE
+          if (it == 0) c_w0 = clock64();
+#endif
           mbar_arrive_expect_tx(&raw_full[s], RAWY + xbytes);
 #ifdef CE_K4_TRACE
           if (it == 0) c_tma0 = clock64();
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         g_k4_trace[size_t(blockIdx.x) * 256 + 200] = c_pdl;
         g_k4_trace[size_t(blockIdx.x) * 256 + 201] = c_dec;
         g_k4_trace[size_t(blockIdx.x) * 256 + 8] = c_tma0;
+        g_k4_trace[size_t(blockIdx.x) * 256 + 204] = c_w0;
       }
 #endif
     }

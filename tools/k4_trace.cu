@@ -99,7 +99,8 @@ int main(int argc, char **argv) {
   names[201] = "producer first decode";
   names[202] = "tmem alloc done";
   names[203] = "barrier init done";
-  for (int slot = 2; slot < 204; ++slot) {
+  names[204] = "producer raw_empty passed";
+  for (int slot = 2; slot < 205; ++slot) {
     if (slot == 5) continue;   // end globaltimer
     std::vector<double> v;
     for (int c = 0; c < nsm; ++c) {
