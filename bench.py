@@ -455,20 +455,6 @@ def run_comb(args):
         torch.cuda.synchronize()
     launches = est.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
-    # practical ceiling for this traffic (outside the timed region): a plain device copy y -> h of the same
-    # bytes over the same rotating buffers, back to back (torch's copy kernel, not ours)
-    copy_steps = min(args.steps, 500)
-    with torch.cuda.stream(stream):
-        for i in range(10):
-            h_dev[i % nbuf].copy_(y_dev[i % nbuf])
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record(stream)
-        for i in range(copy_steps):
-            h_dev[i % nbuf].copy_(y_dev[i % nbuf])
-        c1.record(stream)
-        torch.cuda.synchronize()
-    copy_us = c0.elapsed_time(c1) * 1e3 / copy_steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
