@@ -13,7 +13,8 @@
 //
 // Pipeline (persistent, one CTA per SM, 480 threads):
 //   warp 12   : raw producer -- 2D TMA of the raw y box [128 rows x 16 complex] and the pilot box
-//               [K rows x 16 complex] of each K chunk into a 4-deep raw ring
+//               [K rows x 16 complex] of each K chunk into a 4-deep raw ring (3-deep when the staged
+//               epilogue below takes 16 KB); decodes its first tile while the other warps set up
 //   warps 0-7 : transform -- y and x of 4 rows x 2 tones per thread into registers, LS = y conj(x)/|x|^2,
 //               release the raw slot, bf16 hi/lo -> SWIZZLE_64B K-major A tiles of the 3-deep A/B ring;
 //               fence.proxy.async; arrive a_full
@@ -21,11 +22,14 @@
 //               (pre-swizzled SW64 image)
 //   warp 13   : TMEM allocator + MMA issuer: 2 K-steps x 3 MMAs per chunk, commit -> st_empty;
 //               per tile commit -> tmem_full[acc] (two 256-column accumulators)
-//   warps 8-11: epilogue -- tcgen05.ld 16x256b (4 threads hold 4 consecutive outputs of a row), direct
-//               8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes
+//   warps 8-11: epilogue (epi_block) -- tcgen05.ld 16x256b (4 threads hold 4 consecutive outputs of a
+//               row) per 32-float column block; interior blocks go through SWIZZLE_128B staging and one TMA
+//               store of [32 rows x 128 B] (per-warp staging when CTAs walk several tiles, the idle A/B
+//               ring on a CTA's last tile); window edges / odd starts / ragged tiles use direct 8-byte
+//               stores (8 rows x 32 contiguous bytes per warp instruction)
 // The window table rides in the kernel parameters (no dependent global load before the first TMA), and
 // the kernel is launched with programmatic stream serialization (PDL): its launch overlaps the previous
-// kernel's tail; griddepcontrol.wait precedes every global access.
+// kernel's tail; griddepcontrol.wait precedes every access to caller data.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
