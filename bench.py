@@ -206,9 +206,12 @@ def run_ours(args, cfg):
     r, s2 = workload.channel_stats(cfg, 0)
     soi = workload.set_of_instance(cfg)
     x = workload.gen_pilots(cfg, 0)
-    # weak scaling: the global batch has world*M antennas; rank r owns the contiguous block
-    # [r*M, (r+1)*M) (shard.antenna_shard), drawn with the per-(t, m) seeds of the full draw
-    m_lo, m_hi = antenna_shard(world * cfg.M, world, rank)
+    # weak scaling (default): the global batch has world*M antennas; rank r owns the contiguous block
+    # [r*M, (r+1)*M) (shard.antenna_shard), drawn with the per-(t, m) seeds of the full draw.
+    # --strong: the configuration's own M antennas are split across the ranks (config 5's
+    # 256 antennas on 8 GPUs)
+    M_glob = cfg.M if args.strong else world * cfg.M
+    m_lo, m_hi = antenna_shard(M_glob, world, rank)
     y = workload.gen_instances(cfg, 0, m_lo=m_lo, m_hi=m_hi, x=x)
     est = ce.ChannelEstimator(cfg.N, cfg.b, cfg.stride, r, s2, kernel=args.kernel)
     stream = torch.cuda.current_stream()
@@ -290,8 +293,9 @@ def run_ours(args, cfg):
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_max = float(t_local.item())
-    E = cfg.estimates
-    value = world * E * args.steps / (ms_max * 1e-3)
+    E_glob = cfg.estimates * M_glob // cfg.M          # estimates of the whole job per step
+    E = cfg.estimates * (m_hi - m_lo) // cfg.M        # this rank's estimates per launch (roofline)
+    value = E_glob * args.steps / (ms_max * 1e-3)
     kernel_s = ms / args.steps * 1e-3      # one contraction launch per step on this stream
 
     # end-to-end through the public host-buffer API: pinned host in, pinned host out
@@ -313,7 +317,7 @@ def run_ours(args, cfg):
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * E * e2e_steps / (float(e2e_ms.item()) * 1e-3)
+    e2e_value = E_glob * e2e_steps / (float(e2e_ms.item()) * 1e-3)
 
     # roofline of the dominant kernel (the contraction, one launch per step)
     props = torch.cuda.get_device_properties(dev)
@@ -371,9 +375,9 @@ def run_ours(args, cfg):
     if world > 1 and not args.no_verify:
         try:
             from paper_1802_05427_b200.shard import gather_antenna_shards
-            full = gather_antenna_shards(h_dev[(args.steps - 1) % nbuf], world * cfg.M)
+            full = gather_antenna_shards(h_dev[(args.steps - 1) % nbuf], M_glob)
             if rank == 0:
-                y_all = workload.gen_instances(cfg, 0, m_lo=0, m_hi=world * cfg.M, x=x)
+                y_all = workload.gen_instances(cfg, 0, m_lo=0, m_hi=M_glob, x=x)
                 h_ref = est.estimate(torch.from_numpy(y_all).to(dev), x_dev, set_of_instance=soi_dev)
                 torch.cuda.synchronize()
                 verify = {"nccl_all_gather_bytes": int(full.numel() * 8),
@@ -388,11 +392,12 @@ def run_ours(args, cfg):
         line = {
             "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value, "unit": "estimates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (seeded workload generator, SURVEY.md §8(d) recipe)",
             "config": _cfg_json(cfg, {"l2": f"rotating {nbuf} y/h buffer pairs ({nbuf * step_bytes / 2**20:.0f} MiB > L2)",
                                       "kernel": {0: "auto", 1: "simt", 2: "tf32x3", 3: "bf16x3", 4: "bf16x3_pair"}[args.kernel] + f"->{kname}",
-                                      "global_batch_instances": world * cfg.T,
+                                      "global_antennas": M_glob,
                                       "parallelism": f"antenna/batch shard x{world}"}),
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -565,6 +570,8 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip the N>1 NCCL gather + single-GPU bitwise check")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the configuration's M antennas across the ranks (default: weak, M per rank)")
     ap.add_argument("--stats", action="store_true", help="time the NEXT-3 statistics estimator instead")
     ap.add_argument("--comb", default=None, help="run the comb-pilot 3W/12W path on workload.COMB_CONFIGS[NAME]")
     args = ap.parse_args()

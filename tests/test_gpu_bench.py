@@ -24,6 +24,7 @@ def _run(*args):
 @pytest.mark.parametrize("extra", [
     ["--config", "3"],
     ["--config", "1"],
+    ["--config", "2", "--strong"],
     ["--comb", "paper_12w"],
     ["--comb", "paper_3w"],
     ["--stats"],
