@@ -88,7 +88,7 @@ struct ce_handle {
   // host-buffer pipeline: streams[0] H2D copies, [1] kernels, [2] D2H copies; per-chunk events
   static constexpr int MAX_CHUNKS = 64;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_done[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[MAX_CHUNKS] = {}, ev_out[MAX_CHUNKS] = {};
   int64_t launches = 0;
 };
@@ -141,7 +141,6 @@ void release(ce_handle *h) {
   for (auto &s : h->streams)
     if (s) cudaStreamDestroy(s);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
-  if (h->ev_x) cudaEventDestroy(h->ev_x);
   for (auto &e : h->ev_in)
     if (e) cudaEventDestroy(e);
   for (auto &e : h->ev_out)
@@ -462,7 +461,6 @@ int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void 
   if (h->streams[0] == nullptr) {
     for (auto &s : h->streams) CE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
     CE_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event create");
-    CE_CUDA(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_done) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_in) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_out) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
