@@ -151,7 +151,7 @@ def test_edge_shapes(N, b, s, M, K, T, kernel):
 
 def test_full_band_equals_full_lmmse():
     """NEXT-2: b = N (config 6) is the full N x N LMMSE of Eq. 12-15; the tensor-core path splits its single
-    1200-output window into 124-output sub-windows over the same input range."""
+    1200-output window into 125-128-output sub-windows over the same input range."""
     ce = _ce()
     cfg = CONFIGS[6]
     r, s2, x, y, soi = _inputs(cfg, m_hi=16)
