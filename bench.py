@@ -551,7 +551,9 @@ def run_stats(args):
             "config": _cfg_json(cfg, {"D": D, "B": B, "l2": f"rotating {nbuf} y buffers (> L2)"}),
             "roofline": {"bound": "alu", "achieved": flops / (ms * 1e-3) / 1e12, "peak": fp32_peak / 1e12,
                          "unit": "TFLOP/s", "frac": flops / (ms * 1e-3) / fp32_peak, "traffic": None,
-                         "kernel": "k7_accumulate", "algorithmic_flops_per_launch": flops},
+                         "kernel": "k8_gram (lags, >= 16384 columns) + k7_accumulate", "algorithmic_flops_per_launch": flops,
+                         "note": "whole-step algorithmic flops (lags + noise DFT bins) vs the FP32 SIMT peak; from "
+                                 "16384 columns the lag part runs on the tensor cores (K8), so this is an effective rate"},
             "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "device": props.name}
     print(json.dumps(line), flush=True)
 

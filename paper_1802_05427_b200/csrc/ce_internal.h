@@ -66,6 +66,11 @@ bool pair_launchable(const ContractArgs &a);
 cudaError_t launch_contract_pair(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                  cudaStream_t stream, int64_t *launches);
 
+// K8: the statistics estimator's lag correlation (banded Gram matrix) on tcgen05; adds into K7's accumulator.
+bool gram_launchable(const float2 *y, int32_t K, int32_t N, int32_t D);
+cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, int32_t K, int32_t N,
+                        const int32_t *soi, int32_t n_sets, int32_t D, double *acc, cudaStream_t stream);
+
 void set_last_error(const std::string &msg);
 
 }  // namespace ce

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "ce_internal.h"
@@ -30,14 +32,15 @@ constexpr int LB = 4;          // lags per thread
 
 __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                             int M, int K, int N, const int32_t *__restrict__ soi,
-                                                            int n_sets, int D, int B, double *__restrict__ acc) {
+                                                            int n_sets, int D, int B, double *__restrict__ acc,
+                                                            int lags, int cpb) {
   extern __shared__ float2 sm7[];
   float2 *ls = sm7;                                  // [N]
   float2 *tw = sm7 + N;                              // [N] exp(+j 2 pi n / N)
   __shared__ double part[2 * LB * K7_THREADS];       // [lag in block][thread][re, im]
   const int MK = M * K;
-  const int n_cb = (MK + K7_CPB - 1) / K7_CPB;
-  const int t = blockIdx.x / n_cb, c_lo = (blockIdx.x % n_cb) * K7_CPB, c_hi = min(MK, c_lo + K7_CPB);
+  const int n_cb = (MK + cpb - 1) / cpb;
+  const int t = blockIdx.x / n_cb, c_lo = (blockIdx.x % n_cb) * cpb, c_hi = min(MK, c_lo + cpb);
   const int set = soi ? soi[t] : 0;
   if (set < 0 || set >= n_sets) return;              // out-of-range set: the instance is skipped
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
@@ -49,8 +52,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
   double *acc_s = acc + size_t(set) * (2 * D + 2);   // [re, im] x D lags, noise power, column count
   // lag work split: thread -> (block of LB consecutive lags, n-range); partial sums stay in registers
   // across the CTA's columns and are reduced once at the end
-  const int n_lb = (D + LB - 1) / LB;
-  const int nparts = max(1, int(blockDim.x) / n_lb);
+  const int n_lb = (lags + LB - 1) / LB;               // 0 when K8 computes the lags on the tensor cores
+  const int nparts = max(1, int(blockDim.x) / max(1, n_lb));
   const int lanes = blockDim.x / nparts;
   const int lb = int(threadIdx.x) % lanes, pr = int(threadIdx.x) / lanes;
   const bool lag_thread = lb < n_lb && pr < nparts && lanes >= n_lb;
@@ -114,12 +117,25 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
         const int kap = lo + bi;
         const int chunk = (N + bparts - 1) / bparts;
         const int n0 = bp * chunk, n1 = min(N, n0 + chunk);
-        int idx = int((static_cast<long long>(n0) * kap) % N);   // (n * kap) mod N
-        for (int n = n0; n < n1; ++n) {
-          const float2 w = tw[idx], v = ls[n];
-          nre = fmaf(v.x, w.x, fmaf(-v.y, w.y, nre));
-          nim = fmaf(v.x, w.y, fmaf(v.y, w.x, nim));
-          idx += kap;
+        // the twiddle e^{+j 2 pi n kap / N} advances by a register rotation, re-seeded from the table at the
+        // start of every 32-tone block (FP32 rotation error <= ~32 * 2^-23): the inner loop is one broadcast
+        // shared-memory read (ls[n]) and 8 FP32 operations per tone, no gathers and no index arithmetic
+        const float2 rot = tw[kap % N];
+        const int step32 = int((32LL * kap) % N);
+        int idx = int((static_cast<long long>(n0) * kap) % N);   // (n * kap) mod N at the block start
+        const float2 *lp = ls + n0;
+        for (int nb = n0; nb < n1; nb += 32) {
+          float2 w = tw[idx];
+          const int cnt = min(32, n1 - nb);
+#pragma unroll 4
+          for (int q = 0; q < cnt; ++q) {
+            const float2 v = lp[q];
+            nre = fmaf(v.x, w.x, fmaf(-v.y, w.y, nre));
+            nim = fmaf(v.x, w.y, fmaf(v.y, w.x, nim));
+            w = make_float2(fmaf(w.x, rot.x, -w.y * rot.y), fmaf(w.x, rot.y, w.y * rot.x));
+          }
+          lp += 32;
+          idx += step32;
           if (idx >= N) idx -= N;
         }
       }
@@ -216,7 +232,18 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   if ((reinterpret_cast<uintptr_t>(d_r) | reinterpret_cast<uintptr_t>(d_sigma2) | reinterpret_cast<uintptr_t>(d_work)) & 7u)
     return fail(CE_EINVAL, "ce_stats_estimate: outputs / workspace must be 8-byte aligned");
   const long long cols = (long long)T * M * K;
-  const long long ctas = (long long)T * ((static_cast<long long>(M) * K + ce::K7_CPB - 1) / ce::K7_CPB);
+  // columns per CTA: 1 when K7 also runs the lags (measured: more is slower there); with the lags on K8 the
+  // per-CTA twiddle table and row-load latency are amortised over several columns
+  static const int env_cpb = getenv("CE_K7_CPB") ? atoi(getenv("CE_K7_CPB")) : 0;   // experiments
+  static const int env_gram = getenv("CE_K8_GRAM") ? atoi(getenv("CE_K8_GRAM")) : -1;   // experiments: 0 off, 1 force
+  const bool gram = env_gram != 0;
+  // K8 pays a per-unit factor table and diagonal-bin epilogue: measured faster from config 4's 61440 columns
+  // up (config 4: 2.4 vs 4.1 ms, config 5: 9.7 vs 17.2 ms) and slower on config 3's 1536 (164 vs 147 us)
+  const bool k8 = gram && (cols >= 16384 || env_gram == 1) && ce::gram_launchable(static_cast<const float2 *>(d_y), K, N, D);
+  int cpb = k8 ? 8 : ce::K7_CPB;
+  if (env_cpb > 0) cpb = env_cpb;
+  cpb = std::max(1, std::min(cpb, M * K));
+  const long long ctas = (long long)T * ((static_cast<long long>(M) * K + cpb - 1) / cpb);
   if (cols > 0x7fffffffLL || ctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
   const size_t smem = size_t(2) * N * sizeof(float2);
   if (smem > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large (N <= 12800)");
@@ -229,9 +256,20 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
     return CE_ECUDA;
   }
+  // the lag correlation on the tensor cores (K8) when it fits; K7 then adds the noise floor and column count
+  int k7_lags = D;
+  if (k8) {
+    e = ce::launch_gram(static_cast<const float2 *>(d_y), static_cast<const float2 *>(d_x), T, M, K, N,
+                        d_set_of_instance, n_sets, D, acc, st);
+    if (e != cudaSuccess) {
+      ce::set_last_error(std::string("ce_stats_estimate: K8 launch: ") + cudaGetErrorString(e));
+      return CE_ECUDA;
+    }
+    k7_lags = 0;
+  }
   ce::k7_accumulate<<<unsigned(ctas), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
                                                                   static_cast<const float2 *>(d_x), M, K, N,
-                                                                  d_set_of_instance, n_sets, D, B, acc);
+                                                                  d_set_of_instance, n_sets, D, B, acc, k7_lags, cpb);
   ce::k7_finalize<<<(n_sets + 127) / 128, 128, 0, st>>>(acc, n_sets, N, D, B, static_cast<double *>(d_r),
                                                        static_cast<double *>(d_sigma2));
   e = cudaGetLastError();

@@ -25,12 +25,12 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
+bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows, int box_floats = 32) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cuuint64_t(2) * N, cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(2) * N * 4};
-  cuuint32_t box[2] = {cuuint32_t(32), cuuint32_t(box_rows)};   // 16 complex per box row
+  cuuint32_t box[2] = {cuuint32_t(box_floats), cuuint32_t(box_rows)};   // 16 complex per box row by default
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

@@ -65,3 +65,17 @@ def test_estimated_statistics_drive_the_filters():
     mse = np.mean(np.abs(h.cpu().numpy() - H) ** 2)
     cf = oracle.block_mse(r_true[0], s2_true[0], cfg.b)
     assert mse < 1.10 * cf, (mse, cf)
+
+
+def test_stats_parity_with_k8_forced():
+    """The statistics parity tests again with the tensor-core lag correlation (K8) forced on every shape (by
+    default it runs only from 16384 columns up), in a subprocess: CE_K8_GRAM is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CE_K8_GRAM="1", PYTHONPATH=root)
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "not k8_forced",
+                          os.path.join(root, "tests", "test_gpu_stats.py")], env=env, capture_output=True, text=True,
+                         timeout=900, cwd=root)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
