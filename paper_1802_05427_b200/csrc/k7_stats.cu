@@ -9,10 +9,11 @@
 //   r_hat[d]   = R_hat[d] - sigma2_hat delta[d]
 // The noise window is the B delay bins centred on N/2, far from the channel's delay support (reading D2).
 //
-// K7a: one CTA per K7_CPB columns of one instance: the N twiddles exp(j 2 pi n / N) and, column by column, the LS
-// row in shared memory; threads own blocks of 4 lags (x as many n-ranges as fit in 256 threads, partial sums
-// carried in registers across the columns) and then (bin, n-range) pairs of the noise window; one FP64
-// reduction + atomics per CTA into the per-set accumulators.  K7b: one thread per set normalises.
+// K7a: one CTA per cpb columns of one instance: the N twiddles exp(j 2 pi n / N) and, G columns at a time, the LS
+// rows in shared memory; threads own blocks of 4 lags (x as many n-ranges as fit in 256 threads, partial sums
+// carried in registers across the columns; skipped when K8 computes the lags) and then warps own (column,
+// tone range) with one noise bin per lane (a per-32-tone Horner recursion); one FP64 reduction + atomics per
+// CTA into the per-set accumulators.  K7b: one thread per (set, lag) normalises.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -21,6 +22,7 @@
 #include <string>
 
 #include "ce_internal.h"
+#include "tc_ptx.cuh"
 
 namespace ce {
 namespace {
@@ -30,13 +32,19 @@ constexpr int K7_THREADS = 256;
 constexpr int K7_CPB = 1;      // columns per CTA, same instance (measured on config 3: 1 -> 139 us, 2 -> 143, 8 -> 184)
 constexpr int LB = 4;          // lags per thread
 
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// ls rows are padded with zeros to NP = N rounded up to 32 tones (16-byte aligned, whole 32-tone noise blocks)
 __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                             int M, int K, int N, const int32_t *__restrict__ soi,
                                                             int n_sets, int D, int B, double *__restrict__ acc,
-                                                            int lags, int cpb) {
-  extern __shared__ float2 sm7[];
-  float2 *ls = sm7;                                  // [N]
-  float2 *tw = sm7 + N;                              // [N] exp(+j 2 pi n / N)
+                                                            int lags, int cpb, int G, int noise) {
+  extern __shared__ __align__(16) float2 sm7[];
+  const int NP = (N + 31) & ~31;
+  float2 *ls0 = sm7;                                 // [G][NP] LS rows of the resident columns
+  float2 *tw = sm7 + size_t(G) * NP;                 // [N] exp(+j 2 pi n / N)
   __shared__ double part[2 * LB * K7_THREADS];       // [lag in block][thread][re, im]
   const int MK = M * K;
   const int n_cb = (MK + cpb - 1) / cpb;
@@ -58,98 +66,122 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
   const int lb = int(threadIdx.x) % lanes, pr = int(threadIdx.x) / lanes;
   const bool lag_thread = lb < n_lb && pr < nparts && lanes >= n_lb;
   float re[LB] = {0.f, 0.f, 0.f, 0.f}, im[LB] = {0.f, 0.f, 0.f, 0.f};
-  // noise work split: thread -> (bin, n-range)
+  // noise work split: warp -> (resident column g, 32-tone-block range p), lane -> bin
+  const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+  const int nwarps = int(blockDim.x) >> 5;
+  const int P = max(1, nwarps / G);                  // tone ranges per column
+  const int g_w = warp % G, p_w = warp / G;
+  const int nblk = NP / 32, bchunk = (nblk + P - 1) / P;
+  const int blk0 = min(nblk, p_w * bchunk), blk1 = min(nblk, blk0 + bchunk);
   const int lo = N / 2 - B / 2;
-  const int bparts = max(1, int(blockDim.x) / min(B, int(blockDim.x)));
-  const int bins_per_pass = blockDim.x / bparts;
   double pw = 0;
-  for (int c = c_lo; c < c_hi; ++c) {
-    const float2 *yr = y + (size_t(t) * MK + c) * N;
-    const float2 *xr = x + (size_t(t) * K + c % K) * N;
-    __syncthreads();                                 // previous column's ls fully consumed
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-      const float2 yv = yr[n], xv = xr[n];
-      const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
-      ls[n] = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
+  for (int cg = c_lo; cg < c_hi; cg += G) {
+    const int ng = min(G, c_hi - cg);
+    __syncthreads();                                 // previous group's ls fully consumed
+    for (int g = 0; g < ng; ++g) {
+      const int c = cg + g;
+      const float2 *yr = y + (size_t(t) * MK + c) * N;
+      const float2 *xr = x + (size_t(t) * K + c % K) * N;
+      float2 *ls = ls0 + size_t(g) * NP;
+      for (int n = threadIdx.x; n < NP; n += blockDim.x) {
+        float2 v = make_float2(0.f, 0.f);
+        if (n < N) {
+          const float2 yv = yr[n], xv = xr[n];
+          const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
+          v = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
+        }
+        ls[n] = v;
+      }
     }
     __syncthreads();
     // lags: ls[n] is shared by LB lags and ls[n+d..n+d+LB-1] slides (8 FMA per shared-memory read)
-    for (int l0 = 0; l0 < n_lb; l0 += lanes) {
-      const int lbk = l0 + lb;
-      if (lanes >= n_lb ? lag_thread : (lbk < n_lb && pr < nparts)) {
-        const int d = lbk * LB;
-        const int len = N - d, chunk = (len + nparts - 1) / nparts;
-        const int n0 = pr * chunk, n1 = min(len, n0 + chunk);
-        float2 win[LB];
+    for (int g = 0; g < ng && n_lb > 0; ++g) {
+      const float2 *ls = ls0 + size_t(g) * NP;
+      for (int l0 = 0; l0 < n_lb; l0 += lanes) {
+        const int lbk = l0 + lb;
+        if (lanes >= n_lb ? lag_thread : (lbk < n_lb && pr < nparts)) {
+          const int d = lbk * LB;
+          const int len = N - d, chunk = (len + nparts - 1) / nparts;
+          const int n0 = pr * chunk, n1 = min(len, n0 + chunk);
+          float2 win[LB];
 #pragma unroll
-        for (int i = 0; i < LB; ++i) win[i] = (n0 + d + i < N) ? ls[n0 + d + i] : make_float2(0.f, 0.f);
-        float r4[LB] = {0.f, 0.f, 0.f, 0.f}, i4[LB] = {0.f, 0.f, 0.f, 0.f};
-        for (int n = n0; n < n1; ++n) {
-          const float2 bv = ls[n];
+          for (int i = 0; i < LB; ++i) win[i] = (n0 + d + i < N) ? ls[n0 + d + i] : make_float2(0.f, 0.f);
+          float r4[LB] = {0.f, 0.f, 0.f, 0.f}, i4[LB] = {0.f, 0.f, 0.f, 0.f};
+          for (int n = n0; n < n1; ++n) {
+            const float2 bv = ls[n];
 #pragma unroll
-          for (int i = 0; i < LB; ++i) {             // win[i] = ls[n + d + i] (zero beyond N)
-            r4[i] = fmaf(win[i].x, bv.x, fmaf(win[i].y, bv.y, r4[i]));
-            i4[i] = fmaf(win[i].y, bv.x, fmaf(-win[i].x, bv.y, i4[i]));
+            for (int i = 0; i < LB; ++i) {           // win[i] = ls[n + d + i] (zero beyond N)
+              r4[i] = fmaf(win[i].x, bv.x, fmaf(win[i].y, bv.y, r4[i]));
+              i4[i] = fmaf(win[i].y, bv.x, fmaf(-win[i].x, bv.y, i4[i]));
+            }
+#pragma unroll
+            for (int i = 0; i < LB - 1; ++i) win[i] = win[i + 1];
+            win[LB - 1] = (n + d + LB < N) ? ls[n + d + LB] : make_float2(0.f, 0.f);
           }
+          if (lanes >= n_lb) {
 #pragma unroll
-          for (int i = 0; i < LB - 1; ++i) win[i] = win[i + 1];
-          win[LB - 1] = (n + d + LB < N) ? ls[n + d + LB] : make_float2(0.f, 0.f);
-        }
-        if (lanes >= n_lb) {
-#pragma unroll
-          for (int i = 0; i < LB; ++i) {
-            re[i] += r4[i];
-            im[i] += i4[i];
-          }
-        } else {                                     // D > 4 * 256: no register carry, add directly
-          for (int i = 0; i < LB && d + i < D; ++i) {
-            atomicAdd(&acc_s[2 * (d + i)], double(r4[i]));
-            atomicAdd(&acc_s[2 * (d + i) + 1], double(i4[i]));
+            for (int i = 0; i < LB; ++i) {
+              re[i] += r4[i];
+              im[i] += i4[i];
+            }
+          } else {                                   // D > 4 * 256: no register carry, add directly
+            for (int i = 0; i < LB && d + i < D; ++i) {
+              atomicAdd(&acc_s[2 * (d + i)], double(r4[i]));
+              atomicAdd(&acc_s[2 * (d + i) + 1], double(i4[i]));
+            }
           }
         }
       }
     }
-    // noise window: the complex partial sums of a bin are combined before taking |.|^2
-    for (int b0 = 0; b0 < B; b0 += bins_per_pass) {
-      const int bi = b0 + int(threadIdx.x) % bins_per_pass, bp = int(threadIdx.x) / bins_per_pass;
-      float nre = 0.f, nim = 0.f;
-      if (bi < B && bp < bparts) {
-        const int kap = lo + bi;
-        const int chunk = (N + bparts - 1) / bparts;
-        const int n0 = bp * chunk, n1 = min(N, n0 + chunk);
-        // the twiddle e^{+j 2 pi n kap / N} advances by a register rotation, re-seeded from the table at the
-        // start of every 32-tone block (FP32 rotation error <= ~32 * 2^-23): the inner loop is one broadcast
-        // shared-memory read (ls[n]) and 8 FP32 operations per tone, no gathers and no index arithmetic
-        const float2 rot = tw[kap % N];
-        const int step32 = int((32LL * kap) % N);
-        int idx = int((static_cast<long long>(n0) * kap) % N);   // (n * kap) mod N at the block start
-        const float2 *lp = ls + n0;
-        for (int nb = n0; nb < n1; nb += 32) {
-          float2 w = tw[idx];
-          const int cnt = min(32, n1 - nb);
-#pragma unroll 4
-          for (int q = 0; q < cnt; ++q) {
-            const float2 v = lp[q];
-            nre = fmaf(v.x, w.x, fmaf(-v.y, w.y, nre));
-            nim = fmaf(v.x, w.y, fmaf(v.y, w.x, nim));
-            w = make_float2(fmaf(w.x, rot.x, -w.y * rot.y), fmaf(w.x, rot.y, w.y * rot.x));
+    // noise window X[kap] = sum_n ls[n] e^{+j 2 pi n kap / N}: per 32-tone block a Horner recursion in w = e^{j 2 pi
+    // kap / N} (two chains, even and odd tones, in w^2: 4 FMA per tone, ls read as broadcast 2-tone vectors), the
+    // block's sum rotated by the tabled e^{j 2 pi 32 blk kap / N}; the complex partial sums of a bin are combined
+    // before taking |.|^2
+    const float2 *lsw = ls0 + size_t(g_w) * NP;
+    for (int b0 = 0; b0 < (noise ? B : 0); b0 += 32) {
+      const int bin = b0 + lane;
+      const int kap = lo + min(bin, B - 1);
+      const float2 w1 = tw[kap], w2 = cmulf(w1, w1);
+      const int step = int((32LL * kap) % N);
+      int idx = int((32LL * blk0 * kap) % N);
+      float xr = 0.f, xi = 0.f;
+      if (g_w < ng) {
+        for (int blk = blk0; blk < blk1; ++blk) {
+          const float4 *vp = reinterpret_cast<const float4 *>(lsw + blk * 32);
+          float4 v = vp[15];                         // tones 30 (x, y) and 31 (z, w)
+          float er = v.x, ei = v.y, orr = v.z, oi = v.w;
+#pragma unroll
+          for (int q = 14; q >= 0; --q) {
+            v = vp[q];
+            const float ner = fmaf(er, w2.x, fmaf(-ei, w2.y, v.x));
+            const float nei = fmaf(er, w2.y, fmaf(ei, w2.x, v.y));
+            const float nor = fmaf(orr, w2.x, fmaf(-oi, w2.y, v.z));
+            const float noi = fmaf(orr, w2.y, fmaf(oi, w2.x, v.w));
+            er = ner; ei = nei; orr = nor; oi = noi;
           }
-          lp += 32;
-          idx += step32;
+          const float pr_ = er + fmaf(orr, w1.x, -oi * w1.y), pi_ = ei + fmaf(orr, w1.y, oi * w1.x);
+          const float2 s = tw[idx];
+          xr = fmaf(s.x, pr_, fmaf(-s.y, pi_, xr));
+          xi = fmaf(s.x, pi_, fmaf(s.y, pr_, xi));
+          idx += step;
           if (idx >= N) idx -= N;
         }
       }
-      __syncthreads();                               // part[] free
-      part[2 * threadIdx.x] = nre;
-      part[2 * threadIdx.x + 1] = nim;
-      __syncthreads();
-      if (threadIdx.x < bins_per_pass && b0 + int(threadIdx.x) < B) {
-        double sr = 0, si = 0;
-        for (int q = 0; q < bparts; ++q) {
-          sr += part[2 * (q * bins_per_pass + threadIdx.x)];
-          si += part[2 * (q * bins_per_pass + threadIdx.x) + 1];
+      if (P == 1) {
+        if (bin < B && g_w < ng) pw += double(xr) * xr + double(xi) * xi;
+      } else {
+        __syncthreads();                             // part[] free
+        part[2 * threadIdx.x] = xr;
+        part[2 * threadIdx.x + 1] = xi;
+        __syncthreads();
+        if (p_w == 0 && bin < B && g_w < ng) {
+          double sr = 0, si = 0;
+          for (int q = 0; q < P; ++q) {
+            sr += part[2 * ((q * G + g_w) * 32 + lane)];
+            si += part[2 * ((q * G + g_w) * 32 + lane) + 1];
+          }
+          pw += sr * sr + si * si;
         }
-        pw += sr * sr + si * si;
       }
     }
   }
@@ -174,6 +206,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
       atomicAdd(&acc_s[2 * dd + 1], si);
     }
   }
+  if (!noise) return;                                // K7c adds the noise floor and the column count
   __syncthreads();
   part[threadIdx.x] = pw;
   __syncthreads();
@@ -187,20 +220,166 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
   }
 }
 
+// K7c -- the noise window on its own, streamed: one CTA per (instance t, user k, range of antennas m), so one x
+// row (the LS factors conj(x)/|x|^2) serves all its columns c = (m, k); each warp owns every 8th column of the range
+// and streams that column's y row in 256-tone chunks into its own 3-deep ring by 1-D bulk copies (no CTA barrier
+// in the loop), converts the chunk to LS values in place, then runs the per-32-tone Horner recursion of K7a with
+// one bin per lane (NBG groups of 32 bins per pass over the columns).  Needs N even and y 16-byte aligned (whole
+// 16-byte bulk copies).
+constexpr int NZ_CH = 256;     // tones per chunk
+constexpr int NZ_R = 3;        // chunks in flight per warp
+constexpr int NZ_WARPS = 8;
+
+template <int NBG>
+__global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restrict__ y, const float2 *__restrict__ x,
+                                                          int M, int K, int N, const int32_t *__restrict__ soi,
+                                                          int n_sets, int D, int B, double *__restrict__ acc, int mpb) {
+  extern __shared__ __align__(128) unsigned char smz[];
+  const int nch = (N + NZ_CH - 1) / NZ_CH;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smz);                  // [warp][R]
+  float2 *ring = reinterpret_cast<float2 *>(smz + 1024);               // [warp][R][CH]
+  float2 *fac = ring + NZ_WARPS * NZ_R * NZ_CH;                        // [nch * CH] conj(x)/|x|^2, zero beyond N
+  float2 *tw = fac + size_t(nch) * NZ_CH;                              // [N] exp(+j 2 pi n / N)
+  const int n_mc = (M + mpb - 1) / mpb;
+  const int mc = blockIdx.x % n_mc, tk = blockIdx.x / n_mc, k = tk % K, t = tk / K;
+  const int set = soi ? soi[t] : 0;
+  if (set < 0 || set >= n_sets) return;              // out-of-range set: the instance is skipped
+  const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+  const int MK = M * K;
+  const int m_lo = mc * mpb, m_hi = min(M, m_lo + mpb);
+  const int ncol_w = max(0, (m_hi - m_lo - warp + NZ_WARPS - 1) / NZ_WARPS);
+  const int npass = (B + 32 * NBG - 1) / (32 * NBG);  // bin groups of 32 NBG; the columns are re-streamed per pass
+  const int jpp = ncol_w * nch;                       // jobs per pass
+  const int jobs = npass * jpp;
+  uint64_t *wb = bars + warp * NZ_R;
+  float2 *wr = ring + size_t(warp) * NZ_R * NZ_CH;
+  auto issue = [&](int j) {                          // lane 0: chunk j of this warp's column list into slot j % R
+    const int ch = j % nch, m = m_lo + warp + NZ_WARPS * ((j % jpp) / nch);
+    const float2 *src = y + (size_t(t) * MK + size_t(m) * K + k) * N + size_t(ch) * NZ_CH;
+    const uint32_t bytes = uint32_t(min(NZ_CH, N - ch * NZ_CH)) * 8u;
+    mbar_arrive_expect_tx(&wb[j % NZ_R], bytes);
+    bulk_g2s(wr + (j % NZ_R) * NZ_CH, src, bytes, &wb[j % NZ_R]);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < NZ_R; ++s) mbar_init(&wb[s], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int j = 0; j < min(NZ_R, jobs); ++j) issue(j);
+  const float2 *xr = x + (size_t(t) * K + k) * N;
+  for (int n = threadIdx.x; n < nch * NZ_CH; n += blockDim.x) {
+    float2 f = make_float2(0.f, 0.f);
+    if (n < N) {
+      const float2 xv = xr[n];
+      const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
+      f = make_float2(xv.x * inv, -xv.y * inv);
+    }
+    fac[n] = f;
+  }
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float sv, cv;
+    sincospif(2.0f * float(n) / float(N), &sv, &cv);
+    tw[n] = make_float2(cv, sv);
+  }
+  __syncthreads();
+  const int lo = N / 2 - B / 2;
+  float2 w1[NBG], w2[NBG];
+  int step[NBG], idx[NBG];
+  float xr_[NBG], xi_[NBG];
+  int bin0 = 0;
+  double pw = 0;
+  for (int j = 0; j < jobs; ++j) {
+    const int s = j % NZ_R, ch = j % nch;
+    if (j % jpp == 0) {                              // a pass starts: bins bin0 .. bin0 + 32 NBG - 1
+      bin0 = (j / jpp) * 32 * NBG;
+#pragma unroll
+      for (int g = 0; g < NBG; ++g) {
+        const int kap = lo + min(bin0 + 32 * g + lane, B - 1);
+        w1[g] = tw[kap];
+        w2[g] = cmulf(w1[g], w1[g]);
+        step[g] = int((32LL * kap) % N);
+        idx[g] = 0;
+        xr_[g] = xi_[g] = 0.f;
+      }
+    }
+    mbar_wait(&wb[s], uint32_t(j / NZ_R) & 1u);
+    float2 *rb = wr + s * NZ_CH;
+    const int n0 = ch * NZ_CH, len = min(NZ_CH, N - n0);
+#pragma unroll
+    for (int i = lane; i < NZ_CH; i += 32) {         // LS values in place; zero beyond N (whole 32-tone blocks)
+      float2 v = make_float2(0.f, 0.f);
+      if (i < len) v = cmulf(rb[i], fac[n0 + i]);
+      rb[i] = v;
+    }
+    __syncwarp();
+    const int nb = (len + 31) / 32;
+    for (int bb = 0; bb < nb; ++bb) {
+      const float4 *vp = reinterpret_cast<const float4 *>(rb + bb * 32);
+#pragma unroll
+      for (int g = 0; g < NBG; ++g) {
+        float4 v = vp[15];                           // tones 30 (x, y) and 31 (z, w)
+        float er = v.x, ei = v.y, orr = v.z, oi = v.w;
+#pragma unroll
+        for (int q = 14; q >= 0; --q) {
+          v = vp[q];
+          const float ner = fmaf(er, w2[g].x, fmaf(-ei, w2[g].y, v.x));
+          const float nei = fmaf(er, w2[g].y, fmaf(ei, w2[g].x, v.y));
+          const float nor = fmaf(orr, w2[g].x, fmaf(-oi, w2[g].y, v.z));
+          const float noi = fmaf(orr, w2[g].y, fmaf(oi, w2[g].x, v.w));
+          er = ner; ei = nei; orr = nor; oi = noi;
+        }
+        const float pr_ = er + fmaf(orr, w1[g].x, -oi * w1[g].y), pi_ = ei + fmaf(orr, w1[g].y, oi * w1[g].x);
+        const float2 sv = tw[idx[g]];
+        xr_[g] = fmaf(sv.x, pr_, fmaf(-sv.y, pi_, xr_[g]));
+        xi_[g] = fmaf(sv.x, pi_, fmaf(sv.y, pr_, xi_[g]));
+        idx[g] += step[g];
+        if (idx[g] >= N) idx[g] -= N;
+      }
+    }
+    fence_proxy_async();                             // the in-place writes before the slot's next bulk copy
+    __syncwarp();
+    if (lane == 0 && j + NZ_R < jobs) issue(j + NZ_R);
+    if (ch == nch - 1) {                             // column complete
+#pragma unroll
+      for (int g = 0; g < NBG; ++g) {
+        if (bin0 + 32 * g + lane < B) pw += double(xr_[g]) * xr_[g] + double(xi_[g]) * xi_[g];
+        xr_[g] = xi_[g] = 0.f;
+        idx[g] = 0;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+  __shared__ double wpw[NZ_WARPS];
+  if (lane == 0) wpw[warp] = pw;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0;
+    for (int w = 0; w < NZ_WARPS; ++w) sum += wpw[w];
+    double *acc_s = acc + size_t(set) * (2 * D + 2);
+    atomicAdd(&acc_s[2 * D], sum / N);                // unitary IDFT: |sum|^2 / N
+    atomicAdd(&acc_s[2 * D + 1], double(m_hi - m_lo));
+  }
+}
+
+// one thread per (set, lag), lag D standing for sigma^2
 __global__ void k7_finalize(const double *__restrict__ acc, int n_sets, int N, int D, int B, double *__restrict__ r,
                             double *__restrict__ sigma2) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_sets) return;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n_sets * (D + 1)) return;
+  const int s = int(i / (D + 1)), d = int(i % (D + 1));
   const double *a = acc + size_t(s) * (2 * D + 2);
   const double C = a[2 * D + 1];
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   const double s2 = C > 0 ? a[2 * D] / (C * B) : nan;
-  sigma2[s] = s2;
-  for (int d = 0; d < D; ++d) {
-    const double den = C * (N - d);
-    r[(size_t(s) * D + d) * 2] = C > 0 ? a[2 * d] / den - (d == 0 ? s2 : 0.0) : nan;
-    r[(size_t(s) * D + d) * 2 + 1] = C > 0 ? a[2 * d + 1] / den : nan;
+  if (d == D) {
+    sigma2[s] = s2;
+    return;
   }
+  const double den = C * (N - d);
+  r[(size_t(s) * D + d) * 2] = C > 0 ? a[2 * d] / den - (d == 0 ? s2 : 0.0) : nan;
+  r[(size_t(s) * D + d) * 2 + 1] = C > 0 ? a[2 * d + 1] / den : nan;
 }
 
 }  // namespace
@@ -245,8 +424,12 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   cpb = std::max(1, std::min(cpb, M * K));
   const long long ctas = (long long)T * ((static_cast<long long>(M) * K + cpb - 1) / cpb);
   if (cols > 0x7fffffffLL || ctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
-  const size_t smem = size_t(2) * N * sizeof(float2);
-  if (smem > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large (N <= 12800)");
+  // resident LS rows per CTA (1, 2, 4 or 8: whole warps per column in the noise window), bounded by shared memory
+  const int NP = (N + 31) & ~31;
+  if (size_t(NP + N) * sizeof(float2) > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large (N <= 12800)");
+  int G = 1;
+  while (G < 8 && 2 * G <= cpb && size_t(2 * G * NP + N) * sizeof(float2) <= 200 * 1024) G *= 2;
+  const size_t smem = size_t(G * NP + N) * sizeof(float2);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double *acc = static_cast<double *>(d_work);
   cudaError_t e = cudaMemsetAsync(acc, 0, size_t(n_sets) * (2 * D + 2) * sizeof(double), st);
@@ -267,10 +450,47 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     }
     k7_lags = 0;
   }
-  ce::k7_accumulate<<<unsigned(ctas), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
-                                                                  static_cast<const float2 *>(d_x), M, K, N,
-                                                                  d_set_of_instance, n_sets, D, B, acc, k7_lags, cpb);
-  ce::k7_finalize<<<(n_sets + 127) / 128, 128, 0, st>>>(acc, n_sets, N, D, B, static_cast<double *>(d_r),
+  // the noise window streamed by K7c (N even, y 16-byte aligned; bins in passes of up to 128) when K8 has the
+  // lags, else inside K7a's pass over the LS rows (measured: K7a alone 116 us vs K7a lags + K7c 133 us on config 3;
+  // with K8, config 4 2.15 -> 1.60 ms, config 5 11.9 -> 6.1 ms)
+  static const int env_nz = getenv("CE_K7_NOISE") ? atoi(getenv("CE_K7_NOISE")) : -1;   // experiments: 0 off, 1 force
+  static const int env_mpb = getenv("CE_K7_MPB") ? atoi(getenv("CE_K7_MPB")) : 0;
+  const int nbg = (B + 31) / 32;
+  const bool k7c = (env_nz == 1 || (env_nz != 0 && k7_lags == 0)) && N % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(d_y) & 15u) == 0;
+  if (k7_lags > 0 || !k7c) {
+    ce::k7_accumulate<<<unsigned(ctas), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
+                                                                    static_cast<const float2 *>(d_x), M, K, N,
+                                                                    d_set_of_instance, n_sets, D, B, acc, k7_lags, cpb,
+                                                                    G, k7c ? 0 : 1);
+  }
+  if (k7c) {
+    const int nch = (N + ce::NZ_CH - 1) / ce::NZ_CH;
+    const size_t zsm = 1024 + size_t(ce::NZ_WARPS) * ce::NZ_R * ce::NZ_CH * 8 + size_t(nch) * ce::NZ_CH * 8 + size_t(N) * 8;
+    if (zsm > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large for the noise kernel");
+    // antennas per CTA: enough CTAs for ~4 waves of (2-3 resident per SM), whole warps of columns
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    int mpb = env_mpb > 0 ? env_mpb
+                          : int(std::min<long long>(M, std::max<long long>(8, (cols / (long long)(nsm * 12)) & ~7LL)));
+    mpb = std::max(1, std::min(mpb, M));
+    const long long zctas = (long long)T * K * ((M + mpb - 1) / mpb);
+    if (zctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
+    const void *fn = nbg == 1 ? (const void *)ce::k7_noise<1> : nbg == 2 ? (const void *)ce::k7_noise<2> : (const void *)ce::k7_noise<4>;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(zsm));
+    if (e != cudaSuccess) {
+      ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
+      return CE_ECUDA;
+    }
+    const float2 *yy = static_cast<const float2 *>(d_y), *xx = static_cast<const float2 *>(d_x);
+    if (nbg == 1)
+      ce::k7_noise<1><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
+    else if (nbg == 2)
+      ce::k7_noise<2><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
+    else
+      ce::k7_noise<4><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
+  }
+  ce::k7_finalize<<<unsigned((static_cast<long long>(n_sets) * (D + 1) + 127) / 128), 128, 0, st>>>(acc, n_sets, N, D, B, static_cast<double *>(d_r),
                                                        static_cast<double *>(d_sigma2));
   e = cudaGetLastError();
   if (e != cudaSuccess) {

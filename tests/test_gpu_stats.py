@@ -36,6 +36,35 @@ def test_stats_parity(cfg_id, m_hi):
         assert np.max(np.abs(r_g[s] - r_o)) < 1e-4 * abs(r_o[0]), (s, np.max(np.abs(r_g[s] - r_o)))
 
 
+@pytest.mark.parametrize("cfg_id,m_hi,B", [(3, 16, 32), (3, 16, 100), (2, None, 64), (4, 8, 32), (5, 4, 32),
+                                           (5, 4, 300)])
+def test_stats_parity_noise_windows(cfg_id, m_hi, B):
+    """The bench's noise window (B = 32) and windows of 2-10 groups of 32 bins (K7c runs up to 128 bins per pass
+    over the columns, masking the last group)."""
+    cfg = CONFIGS[cfg_id]
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x, m_hi=m_hi)
+    soi = workload.set_of_instance(cfg)
+    D = min(cfg.b, 64)
+    r_g, s2_g = _gpu_stats(y, x, D, B, soi, cfg.n_sets)
+    for s in range(cfg.n_sets):
+        sel = soi == s
+        r_o, s2_o = oracle.estimate_stats(y[sel], x[sel], D, B)
+        assert abs(s2_g[s] / s2_o - 1) < 1e-4, (s, s2_g[s], s2_o)
+        assert np.max(np.abs(r_g[s] - r_o)) < 1e-4 * abs(r_o[0]), (s, np.max(np.abs(r_g[s] - r_o)))
+
+
+def test_stats_parity_odd_tone_count():
+    """N odd: no 16-byte bulk copies, the noise window runs inside K7a."""
+    cfg = dataclasses.replace(CONFIGS[2], N=299, b=40, stride=20)
+    x = workload.gen_pilots(cfg, 0)
+    y = workload.gen_instances(cfg, 0, x=x)
+    r_g, s2_g = _gpu_stats(y, x, 40, 32)
+    r_o, s2_o = oracle.estimate_stats(y, x, 40, 32)
+    assert abs(s2_g[0] / s2_o - 1) < 1e-4
+    assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0])
+
+
 def test_stats_skipped_and_empty_sets():
     cfg = CONFIGS[2]
     x = workload.gen_pilots(cfg, 0)
@@ -67,15 +96,19 @@ def test_estimated_statistics_drive_the_filters():
     assert mse < 1.10 * cf, (mse, cf)
 
 
-def test_stats_parity_with_k8_forced():
-    """The statistics parity tests again with the tensor-core lag correlation (K8) forced on every shape (by
-    default it runs only from 16384 columns up), in a subprocess: CE_K8_GRAM is read once per process."""
+@pytest.mark.parametrize("env", [{"CE_K8_GRAM": "1"}, {"CE_K8_GRAM": "0", "CE_K7_NOISE": "0"},
+                                 {"CE_K8_GRAM": "0", "CE_K7_NOISE": "1"}], ids=["k8_forced", "k7a_only", "k7a_k7c"])
+def test_stats_parity_other_kernel_paths(env):
+    """The statistics parity tests again (i) with the tensor-core lag correlation (K8) forced on every shape (by
+    default it runs only from 16384 columns up; K7c then streams the noise window), (ii) with K7a alone (lags and
+    noise window in one pass, K8 and K7c off), (iii) K7a lags + K7c noise window, in a subprocess: the variables
+    are read once per process."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CE_K8_GRAM="1", PYTHONPATH=root)
-    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "not k8_forced",
+    env = dict(os.environ, PYTHONPATH=root, **env)
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "not other_kernel_paths",
                           os.path.join(root, "tests", "test_gpu_stats.py")], env=env, capture_output=True, text=True,
                          timeout=900, cwd=root)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
