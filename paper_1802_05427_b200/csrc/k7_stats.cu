@@ -36,6 +36,35 @@ __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 
+// packed FP32x2 (FFMA2): one instruction per complex multiply-add half, the scalar operand broadcast
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// z * w + v for complex z, w, v packed (re, im): w given as wab = (w.re, w.im), wba = (-w.im, w.re)
+__device__ __forceinline__ uint64_t cmac2(uint64_t z, uint64_t wab, uint64_t wba, uint64_t v) {
+  const float2 zf = upk2(z);
+  return fma2(pk2(zf.x, zf.x), wab, fma2(pk2(zf.y, zf.y), wba, v));
+}
+
+// e^{+j 2 pi r / N} for 0 <= r < N (the exact integer reduction keeps the FP32 argument 2r/N in [0, 2))
+__device__ __forceinline__ float2 twiddle(int r, int N) {
+  float sv, cv;
+  sincospif(2.0f * float(r) / float(N), &sv, &cv);
+  return make_float2(cv, sv);
+}
+
 // ls rows are padded with zeros to NP = N rounded up to 32 tones (16-byte aligned, whole 32-tone noise blocks)
 __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                             int M, int K, int N, const int32_t *__restrict__ soi,
@@ -221,25 +250,28 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
 }
 
 // K7c -- the noise window on its own, streamed: one CTA per (instance t, user k, range of antennas m), so one x
-// row (the LS factors conj(x)/|x|^2) serves all its columns c = (m, k); each warp owns every 8th column of the range
-// and streams that column's y row in 256-tone chunks into its own 3-deep ring by 1-D bulk copies (no CTA barrier
-// in the loop), converts the chunk to LS values in place, then runs the per-32-tone Horner recursion of K7a with
-// one bin per lane (NBG groups of 32 bins per pass over the columns).  Needs N even and y 16-byte aligned (whole
-// 16-byte bulk copies).
-constexpr int NZ_CH = 256;     // tones per chunk
-constexpr int NZ_R = 3;        // chunks in flight per warp
+// row (the LS factors conj(x)/|x|^2) serves all its columns c = (m, k).  Each warp owns every 8th group of 4
+// columns of the range and streams the group's y rows in 128-tone chunks into its own 2-deep ring by 1-D bulk
+// copies (no CTA barrier in the loop), converts the chunk to LS values in place, then runs a per-32-tone Horner
+// recursion: lane l works on column l / 8 of the group and on NB bins (l % 8) + 8 j, so every broadcast 2-tone
+// shared-memory read (a quarter-warp per column) feeds 4 NB FMAs -- broadcast 16-byte reads cost one wavefront
+// per quarter-warp, so one bin per lane left the kernel bound by shared-memory wavefronts.  Bins beyond 8 NB run
+// in further passes over the columns.  Needs N even and y 16-byte aligned (whole 16-byte bulk copies).
+constexpr int NZ_CH = 128;     // tones per chunk
+constexpr int NZ_CPW = 4;      // columns per warp job
+constexpr int NZ_R = 2;        // chunks in flight per warp
 constexpr int NZ_WARPS = 8;
+constexpr int NZ_NB = 4;       // bins per lane per pass (8 NB bins per pass)
 
-template <int NBG>
 __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                           int M, int K, int N, const int32_t *__restrict__ soi,
                                                           int n_sets, int D, int B, double *__restrict__ acc, int mpb) {
+  constexpr int NB = NZ_NB;
   extern __shared__ __align__(128) unsigned char smz[];
   const int nch = (N + NZ_CH - 1) / NZ_CH;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smz);                  // [warp][R]
-  float2 *ring = reinterpret_cast<float2 *>(smz + 1024);               // [warp][R][CH]
-  float2 *fac = ring + NZ_WARPS * NZ_R * NZ_CH;                        // [nch * CH] conj(x)/|x|^2, zero beyond N
-  float2 *tw = fac + size_t(nch) * NZ_CH;                              // [N] exp(+j 2 pi n / N)
+  float2 *ring = reinterpret_cast<float2 *>(smz + 1024);               // [warp][R][CPW][CH]
+  float2 *fac = ring + NZ_WARPS * NZ_R * NZ_CPW * NZ_CH;               // [nch * CH] conj(x)/|x|^2, zero beyond N
   const int n_mc = (M + mpb - 1) / mpb;
   const int mc = blockIdx.x % n_mc, tk = blockIdx.x / n_mc, k = tk % K, t = tk / K;
   const int set = soi ? soi[t] : 0;
@@ -247,18 +279,23 @@ __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restri
   const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
   const int MK = M * K;
   const int m_lo = mc * mpb, m_hi = min(M, m_lo + mpb);
-  const int ncol_w = max(0, (m_hi - m_lo - warp + NZ_WARPS - 1) / NZ_WARPS);
-  const int npass = (B + 32 * NBG - 1) / (32 * NBG);  // bin groups of 32 NBG; the columns are re-streamed per pass
-  const int jpp = ncol_w * nch;                       // jobs per pass
+  const int ngrp = (m_hi - m_lo + NZ_CPW - 1) / NZ_CPW;
+  const int ngrp_w = max(0, (ngrp - warp + NZ_WARPS - 1) / NZ_WARPS);
+  const int npass = (B + 8 * NB - 1) / (8 * NB);     // bins per pass 8 NB; the columns are re-streamed per pass
+  const int jpp = ngrp_w * nch;                       // jobs (column group, chunk) per pass
   const int jobs = npass * jpp;
   uint64_t *wb = bars + warp * NZ_R;
-  float2 *wr = ring + size_t(warp) * NZ_R * NZ_CH;
-  auto issue = [&](int j) {                          // lane 0: chunk j of this warp's column list into slot j % R
-    const int ch = j % nch, m = m_lo + warp + NZ_WARPS * ((j % jpp) / nch);
-    const float2 *src = y + (size_t(t) * MK + size_t(m) * K + k) * N + size_t(ch) * NZ_CH;
+  float2 *wr = ring + size_t(warp) * NZ_R * NZ_CPW * NZ_CH;
+  auto issue = [&](int j) {                          // lane 0: job j into slot j % R
+    const int ch = j % nch, m0 = m_lo + NZ_CPW * (warp + NZ_WARPS * ((j % jpp) / nch));
+    const int nv = min(NZ_CPW, m_hi - m0);
     const uint32_t bytes = uint32_t(min(NZ_CH, N - ch * NZ_CH)) * 8u;
-    mbar_arrive_expect_tx(&wb[j % NZ_R], bytes);
-    bulk_g2s(wr + (j % NZ_R) * NZ_CH, src, bytes, &wb[j % NZ_R]);
+    uint64_t *bar = &wb[j % NZ_R];
+    mbar_arrive_expect_tx(bar, bytes * uint32_t(nv));
+    for (int i = 0; i < nv; ++i) {
+      const float2 *src = y + (size_t(t) * MK + size_t(m0 + i) * K + k) * N + size_t(ch) * NZ_CH;
+      bulk_g2s(wr + ((j % NZ_R) * NZ_CPW + i) * NZ_CH, src, bytes, bar);
+    }
   };
   if (lane == 0) {
     for (int s = 0; s < NZ_R; ++s) mbar_init(&wb[s], 1);
@@ -277,75 +314,94 @@ __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restri
     }
     fac[n] = f;
   }
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    float sv, cv;
-    sincospif(2.0f * float(n) / float(N), &sv, &cv);
-    tw[n] = make_float2(cv, sv);
-  }
   __syncthreads();
   const int lo = N / 2 - B / 2;
-  float2 w1[NBG], w2[NBG];
-  int step[NBG], idx[NBG];
-  float xr_[NBG], xi_[NBG];
+  const int ci = lane >> 3, bl = lane & 7;            // column of the group, bin lane
+  float2 w1[NB], w32[NB];
+  uint64_t w2ab[NB], w2ba[NB];
+  int kap[NB];
+  float xr_[NB], xi_[NB];
+  float2 rot[NB];
   int bin0 = 0;
   double pw = 0;
   for (int j = 0; j < jobs; ++j) {
     const int s = j % NZ_R, ch = j % nch;
-    if (j % jpp == 0) {                              // a pass starts: bins bin0 .. bin0 + 32 NBG - 1
-      bin0 = (j / jpp) * 32 * NBG;
+    if (j % jpp == 0) {                              // a pass starts: bins bin0 .. bin0 + 8 NB - 1
+      bin0 = (j / jpp) * 8 * NB;
 #pragma unroll
-      for (int g = 0; g < NBG; ++g) {
-        const int kap = lo + min(bin0 + 32 * g + lane, B - 1);
-        w1[g] = tw[kap];
-        w2[g] = cmulf(w1[g], w1[g]);
-        step[g] = int((32LL * kap) % N);
-        idx[g] = 0;
+      for (int g = 0; g < NB; ++g) {
+        kap[g] = lo + min(bin0 + bl + 8 * g, B - 1);
+        w1[g] = twiddle(kap[g], N);
+        const float2 w2 = cmulf(w1[g], w1[g]);
+        w2ab[g] = pk2(w2.x, w2.y);
+        w2ba[g] = pk2(-w2.y, w2.x);
+        w32[g] = twiddle(int((32LL * kap[g]) % N), N);
         xr_[g] = xi_[g] = 0.f;
       }
     }
     mbar_wait(&wb[s], uint32_t(j / NZ_R) & 1u);
-    float2 *rb = wr + s * NZ_CH;
+    float2 *rb = wr + s * NZ_CPW * NZ_CH;
+    const int m0 = m_lo + NZ_CPW * (warp + NZ_WARPS * ((j % jpp) / nch));
+    const int nv = min(NZ_CPW, m_hi - m0);
     const int n0 = ch * NZ_CH, len = min(NZ_CH, N - n0);
-#pragma unroll
-    for (int i = lane; i < NZ_CH; i += 32) {         // LS values in place; zero beyond N (whole 32-tone blocks)
-      float2 v = make_float2(0.f, 0.f);
-      if (i < len) v = cmulf(rb[i], fac[n0 + i]);
-      rb[i] = v;
+#pragma unroll 4
+    for (int e = 2 * lane; e < NZ_CPW * NZ_CH; e += 64) {   // LS values in place, 2 tones per access (len is even);
+      const int i = e / NZ_CH, nn = e % NZ_CH;              // zero beyond N and for absent columns
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < nv && nn < len) {
+        const float4 r = *reinterpret_cast<const float4 *>(rb + e), f = *reinterpret_cast<const float4 *>(fac + n0 + nn);
+        const float2 a = cmulf(make_float2(r.x, r.y), make_float2(f.x, f.y)), b = cmulf(make_float2(r.z, r.w), make_float2(f.z, f.w));
+        v = make_float4(a.x, a.y, b.x, b.y);
+      }
+      *reinterpret_cast<float4 *>(rb + e) = v;
     }
     __syncwarp();
     const int nb = (len + 31) / 32;
+    const float2 *rc = rb + ci * NZ_CH;
+    // rot = e^{j 2 pi n kap / N} at the block start n: 1 at the column start, advanced by e^{j 2 pi 32 kap / N} per
+    // block and re-seeded exactly every 8 chunks (at most 32 FP32 rotation steps between exact values)
+    if (ch % 8 == 0) {
+#pragma unroll
+      for (int g = 0; g < NB; ++g)
+        rot[g] = ch == 0 ? make_float2(1.f, 0.f) : twiddle(int((static_cast<long long>(n0) * kap[g]) % N), N);
+    }
     for (int bb = 0; bb < nb; ++bb) {
-      const float4 *vp = reinterpret_cast<const float4 *>(rb + bb * 32);
+      const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(rc + bb * 32);   // (tone 2q, tone 2q+1)
+      uint64_t ev[NB], od[NB];                       // even / odd tone chains, packed (re, im)
+      ulonglong2 v = vp[15];                         // tones 30 and 31
 #pragma unroll
-      for (int g = 0; g < NBG; ++g) {
-        float4 v = vp[15];                           // tones 30 (x, y) and 31 (z, w)
-        float er = v.x, ei = v.y, orr = v.z, oi = v.w;
+      for (int g = 0; g < NB; ++g) {
+        ev[g] = v.x;
+        od[g] = v.y;
+      }
 #pragma unroll
-        for (int q = 14; q >= 0; --q) {
-          v = vp[q];
-          const float ner = fmaf(er, w2[g].x, fmaf(-ei, w2[g].y, v.x));
-          const float nei = fmaf(er, w2[g].y, fmaf(ei, w2[g].x, v.y));
-          const float nor = fmaf(orr, w2[g].x, fmaf(-oi, w2[g].y, v.z));
-          const float noi = fmaf(orr, w2[g].y, fmaf(oi, w2[g].x, v.w));
-          er = ner; ei = nei; orr = nor; oi = noi;
+      for (int q = 14; q >= 0; --q) {
+        v = vp[q];
+#pragma unroll
+        for (int g = 0; g < NB; ++g) {
+          ev[g] = cmac2(ev[g], w2ab[g], w2ba[g], v.x);
+          od[g] = cmac2(od[g], w2ab[g], w2ba[g], v.y);
         }
-        const float pr_ = er + fmaf(orr, w1[g].x, -oi * w1[g].y), pi_ = ei + fmaf(orr, w1[g].y, oi * w1[g].x);
-        const float2 sv = tw[idx[g]];
+      }
+#pragma unroll
+      for (int g = 0; g < NB; ++g) {
+        const float2 e2 = upk2(ev[g]), o2 = upk2(od[g]);
+        const float pr_ = e2.x + fmaf(o2.x, w1[g].x, -o2.y * w1[g].y);
+        const float pi_ = e2.y + fmaf(o2.x, w1[g].y, o2.y * w1[g].x);
+        const float2 sv = rot[g];
         xr_[g] = fmaf(sv.x, pr_, fmaf(-sv.y, pi_, xr_[g]));
         xi_[g] = fmaf(sv.x, pi_, fmaf(sv.y, pr_, xi_[g]));
-        idx[g] += step[g];
-        if (idx[g] >= N) idx[g] -= N;
+        rot[g] = cmulf(rot[g], w32[g]);
       }
     }
     fence_proxy_async();                             // the in-place writes before the slot's next bulk copy
     __syncwarp();
     if (lane == 0 && j + NZ_R < jobs) issue(j + NZ_R);
-    if (ch == nch - 1) {                             // column complete
+    if (ch == nch - 1) {                             // the group's columns complete
 #pragma unroll
-      for (int g = 0; g < NBG; ++g) {
-        if (bin0 + 32 * g + lane < B) pw += double(xr_[g]) * xr_[g] + double(xi_[g]) * xi_[g];
+      for (int g = 0; g < NB; ++g) {
+        if (ci < nv && bin0 + bl + 8 * g < B) pw += double(xr_[g]) * xr_[g] + double(xi_[g]) * xi_[g];
         xr_[g] = xi_[g] = 0.f;
-        idx[g] = 0;
       }
     }
   }
@@ -450,12 +506,11 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     }
     k7_lags = 0;
   }
-  // the noise window streamed by K7c (N even, y 16-byte aligned; bins in passes of up to 128) when K8 has the
+  // the noise window streamed by K7c (N even, y 16-byte aligned; bins in passes of 32) when K8 has the
   // lags, else inside K7a's pass over the LS rows (measured: K7a alone 116 us vs K7a lags + K7c 133 us on config 3;
   // with K8, config 4 2.15 -> 1.60 ms, config 5 11.9 -> 6.1 ms)
   static const int env_nz = getenv("CE_K7_NOISE") ? atoi(getenv("CE_K7_NOISE")) : -1;   // experiments: 0 off, 1 force
   static const int env_mpb = getenv("CE_K7_MPB") ? atoi(getenv("CE_K7_MPB")) : 0;
-  const int nbg = (B + 31) / 32;
   const bool k7c = (env_nz == 1 || (env_nz != 0 && k7_lags == 0)) && N % 2 == 0 &&
                    (reinterpret_cast<uintptr_t>(d_y) & 15u) == 0;
   if (k7_lags > 0 || !k7c) {
@@ -466,29 +521,24 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   }
   if (k7c) {
     const int nch = (N + ce::NZ_CH - 1) / ce::NZ_CH;
-    const size_t zsm = 1024 + size_t(ce::NZ_WARPS) * ce::NZ_R * ce::NZ_CH * 8 + size_t(nch) * ce::NZ_CH * 8 + size_t(N) * 8;
+    const size_t zsm = 1024 + size_t(ce::NZ_WARPS) * ce::NZ_R * ce::NZ_CPW * ce::NZ_CH * 8 + size_t(nch) * ce::NZ_CH * 8;
     if (zsm > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large for the noise kernel");
-    // antennas per CTA: enough CTAs for ~4 waves of (2-3 resident per SM), whole warps of columns
+    // antennas per CTA: enough CTAs for several waves, whole warps of 4-column groups
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     int mpb = env_mpb > 0 ? env_mpb
-                          : int(std::min<long long>(M, std::max<long long>(8, (cols / (long long)(nsm * 12)) & ~7LL)));
+                          : int(std::min<long long>(M, std::max<long long>(32, (cols / (long long)(nsm * 12)) & ~31LL)));
     mpb = std::max(1, std::min(mpb, M));
     const long long zctas = (long long)T * K * ((M + mpb - 1) / mpb);
     if (zctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
-    const void *fn = nbg == 1 ? (const void *)ce::k7_noise<1> : nbg == 2 ? (const void *)ce::k7_noise<2> : (const void *)ce::k7_noise<4>;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(zsm));
+    e = cudaFuncSetAttribute(ce::k7_noise, cudaFuncAttributeMaxDynamicSharedMemorySize, int(zsm));
     if (e != cudaSuccess) {
       ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
       return CE_ECUDA;
     }
-    const float2 *yy = static_cast<const float2 *>(d_y), *xx = static_cast<const float2 *>(d_x);
-    if (nbg == 1)
-      ce::k7_noise<1><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
-    else if (nbg == 2)
-      ce::k7_noise<2><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
-    else
-      ce::k7_noise<4><<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(yy, xx, M, K, N, d_set_of_instance, n_sets, D, B, acc, mpb);
+    ce::k7_noise<<<unsigned(zctas), ce::NZ_WARPS * 32, zsm, st>>>(static_cast<const float2 *>(d_y),
+                                                                  static_cast<const float2 *>(d_x), M, K, N,
+                                                                  d_set_of_instance, n_sets, D, B, acc, mpb);
   }
   ce::k7_finalize<<<unsigned((static_cast<long long>(n_sets) * (D + 1) + 127) / 128), 128, 0, st>>>(acc, n_sets, N, D, B, static_cast<double *>(d_r),
                                                        static_cast<double *>(d_sigma2));

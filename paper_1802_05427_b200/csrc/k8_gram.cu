@@ -207,14 +207,18 @@ __global__ void __launch_bounds__(K8_THREADS, 1)
           const int ch = 2 * hc + h;
           *reinterpret_cast<uint4 *>(pah + sw64_off(n, ch)) = make_uint4(ah[4 * h], ah[4 * h + 1], ah[4 * h + 2], ah[4 * h + 3]);
           *reinterpret_cast<uint4 *>(pal + sw64_off(n, ch)) = make_uint4(al[4 * h], al[4 * h + 1], al[4 * h + 2], al[4 * h + 3]);
-          *reinterpret_cast<uint4 *>(pbh + sw64_off(2 * n, ch)) =
-              make_uint4(b0h[4 * h], b0h[4 * h + 1], b0h[4 * h + 2], b0h[4 * h + 3]);
-          *reinterpret_cast<uint4 *>(pbl + sw64_off(2 * n, ch)) =
-              make_uint4(b0l[4 * h], b0l[4 * h + 1], b0l[4 * h + 2], b0l[4 * h + 3]);
-          *reinterpret_cast<uint4 *>(pbh + sw64_off(2 * n + 1, ch)) =
-              make_uint4(b1h[4 * h], b1h[4 * h + 1], b1h[4 * h + 2], b1h[4 * h + 3]);
-          *reinterpret_cast<uint4 *>(pbl + sw64_off(2 * n + 1, ch)) =
-              make_uint4(b1l[4 * h], b1l[4 * h + 1], b1l[4 * h + 2], b1l[4 * h + 3]);
+          // rows 2n and 2n+1: lanes with n & 4 store the odd row first, so each quarter-warp's 16-byte stores
+          // cover both 64-byte halves of the 128-byte bank window (all rows 2n sit in the lower half)
+          const uint4 e0h = make_uint4(b0h[4 * h], b0h[4 * h + 1], b0h[4 * h + 2], b0h[4 * h + 3]);
+          const uint4 e0l = make_uint4(b0l[4 * h], b0l[4 * h + 1], b0l[4 * h + 2], b0l[4 * h + 3]);
+          const uint4 e1h = make_uint4(b1h[4 * h], b1h[4 * h + 1], b1h[4 * h + 2], b1h[4 * h + 3]);
+          const uint4 e1l = make_uint4(b1l[4 * h], b1l[4 * h + 1], b1l[4 * h + 2], b1l[4 * h + 3]);
+          const bool sw = (n & 4) != 0;
+          const int r0 = 2 * n + (sw ? 1 : 0), r1 = 2 * n + (sw ? 0 : 1);
+          *reinterpret_cast<uint4 *>(pbh + sw64_off(r0, ch)) = sw ? e1h : e0h;
+          *reinterpret_cast<uint4 *>(pbl + sw64_off(r0, ch)) = sw ? e1l : e0l;
+          *reinterpret_cast<uint4 *>(pbh + sw64_off(r1, ch)) = sw ? e0h : e1h;
+          *reinterpret_cast<uint4 *>(pbl + sw64_off(r1, ch)) = sw ? e0l : e1l;
         }
         fence_proxy_async();
         mbar_arrive(&a_full[sa]);
