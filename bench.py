@@ -541,20 +541,29 @@ def run_stats(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     samples = cfg.T * cfg.M * cfg.K * cfg.N
     cols = cfg.T * cfg.M * cfg.K
-    flops = 8.0 * cols * (sum(cfg.N - d for d in range(D)) + cfg.N * B)
+    lag_flops = 8.0 * cols * sum(cfg.N - d for d in range(D))
+    noise_flops = 8.0 * cols * cfg.N * B
+    flops = lag_flops + noise_flops
     props = torch.cuda.get_device_properties(0)
     fp32_peak = props.multi_processor_count * 128 * 2 * 1965e6
+    # the library's policy (k7_stats.cu): lags on the tensor cores (K8, BF16x3) from 16384 columns, noise window then
+    # streamed by K7c; below, K7a does both on the FP32 pipes
+    k8 = cols >= 16384 and cfg.K <= 24 and D <= 512 and cfg.N % 2 == 0
+    bf16 = _peaks().get("bf16_tflops", 1605.7) * 1e12
+    t_ideal = (lag_flops / (bf16 / 3) + noise_flops / fp32_peak) if k8 else flops / fp32_peak
     line = {"metric": "LS samples/s through the statistics estimator (NEXT-3)", "value": samples / (ms * 1e-3),
             "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded workload generator)",
             "config": _cfg_json(cfg, {"D": D, "B": B, "l2": f"rotating {nbuf} y buffers (> L2)"}),
-            "roofline": {"bound": "alu", "achieved": flops / (ms * 1e-3) / 1e12, "peak": fp32_peak / 1e12,
-                         "unit": "TFLOP/s", "frac": flops / (ms * 1e-3) / fp32_peak, "traffic": None,
-                         "kernel": "k8_gram (lags, >= 16384 columns) + k7_accumulate", "algorithmic_flops_per_launch": flops,
-                         "note": "whole-step algorithmic flops (lags + noise DFT bins) vs the FP32 SIMT peak; from "
-                                 "16384 columns the lag part runs on the tensor cores (K8), so this is an effective rate"},
-            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "device": props.name}
+            "roofline": {"bound": "tensor+alu" if k8 else "alu", "achieved": flops / (ms * 1e-3) / 1e12,
+                         "peak": flops / t_ideal / 1e12, "unit": "TFLOP/s", "frac": t_ideal / (ms * 1e-3),
+                         "traffic": None, "roofline_time_us": t_ideal * 1e6,
+                         "kernel": "k8_gram (lags) + k7_noise (noise window)" if k8 else "k7_accumulate",
+                         "algorithmic_flops_per_launch": flops,
+                         "note": ("effective peak of the mix: lag flops at the BF16 peak / 3 (BF16x3) plus noise-window "
+                                  "flops at the FP32 SIMT peak" if k8 else "lag + noise-window flops vs the FP32 SIMT peak")},
+            "gpu_launches": (3 if k8 else 2) * args.steps, "clocks": clk.summary(), "device": props.name}
     print(json.dumps(line), flush=True)
 
 
