@@ -167,6 +167,21 @@ __global__ void __launch_bounds__(256) k6_estimate(const float2 *__restrict__ y,
 // register-held LS values with warp-broadcast weight reads) or one estimated tone (3W), the row is staged
 // in shared memory and written out coalesced (3W: with the zero-order hold applied on the way out).
 constexpr int RB = 4;
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {   // a * b + c, FP32x2
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 template <int MODE, int GG, int SS>
 __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                      const float2 *__restrict__ W, float2 *__restrict__ h,
@@ -214,23 +229,22 @@ __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ 
     const int q0 = MODE == 0 ? 0 : e % GG, q1 = MODE == 0 ? n_out : q0 + 1;
     for (int q = q0; q < q1; ++q) {
       const float2 *w = Ws + ((gq - a) * n_out + q) * GG;
-      float re[RB], im[RB];
+      // packed FP32x2 complex MACs: (re, im) += l.x (w.re, w.im) + l.y (-w.im, w.re), two FFMA2 per MAC with the
+      // l components as broadcast scalar operands (half the issue slots of four FFMA)
+      uint64_t acc[RB];
 #pragma unroll
-      for (int r = 0; r < RB; ++r) re[r] = im[r] = 0.f;
+      for (int r = 0; r < RB; ++r) acc[r] = 0ull;
 #pragma unroll
       for (int j = 0; j < GG; ++j) {
         const float2 wv = w[j];
+        const uint64_t wab = pk2(wv.x, wv.y), wba = pk2(-wv.y, wv.x);
 #pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          re[r] = fmaf(wv.x, l[r][j].x, re[r]);
-          re[r] = fmaf(-wv.y, l[r][j].y, re[r]);
-          im[r] = fmaf(wv.x, l[r][j].y, im[r]);
-          im[r] = fmaf(wv.y, l[r][j].x, im[r]);
-        }
+        for (int r = 0; r < RB; ++r)
+          acc[r] = fma2(pk2(l[r][j].x, l[r][j].x), wab, fma2(pk2(l[r][j].y, l[r][j].y), wba, acc[r]));
       }
 #pragma unroll
       for (int r = 0; r < RB; ++r)
-        outs[r * per_row + (MODE == 0 ? q * (K + 1) + gq : e)] = make_float2(re[r], im[r]);
+        outs[r * per_row + (MODE == 0 ? q * (K + 1) + gq : e)] = upk2(acc[r]);
     }
   }
   __syncthreads();
