@@ -135,17 +135,25 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
           float2 win[LB];
 #pragma unroll
           for (int i = 0; i < LB; ++i) win[i] = (n0 + d + i < N) ? ls[n0 + d + i] : make_float2(0.f, 0.f);
-          float r4[LB] = {0.f, 0.f, 0.f, 0.f}, i4[LB] = {0.f, 0.f, 0.f, 0.f};
+          // packed FFMA2: acc = (re, -im) of sum win * conj(b) += win.x (b.x, b.y) + win.y (b.y, -b.x); the two
+          // packed forms of b are shared by the LB lags, the window components are broadcast scalar operands
+          uint64_t acc4[LB] = {0ull, 0ull, 0ull, 0ull};
           for (int n = n0; n < n1; ++n) {
             const float2 bv = ls[n];
+            const uint64_t bab = pk2(bv.x, bv.y), bba = pk2(bv.y, -bv.x);
 #pragma unroll
-            for (int i = 0; i < LB; ++i) {           // win[i] = ls[n + d + i] (zero beyond N)
-              r4[i] = fmaf(win[i].x, bv.x, fmaf(win[i].y, bv.y, r4[i]));
-              i4[i] = fmaf(win[i].y, bv.x, fmaf(-win[i].x, bv.y, i4[i]));
-            }
+            for (int i = 0; i < LB; ++i)             // win[i] = ls[n + d + i] (zero beyond N)
+              acc4[i] = fma2(pk2(win[i].x, win[i].x), bab, fma2(pk2(win[i].y, win[i].y), bba, acc4[i]));
 #pragma unroll
             for (int i = 0; i < LB - 1; ++i) win[i] = win[i + 1];
             win[LB - 1] = (n + d + LB < N) ? ls[n + d + LB] : make_float2(0.f, 0.f);
+          }
+          float r4[LB], i4[LB];
+#pragma unroll
+          for (int i = 0; i < LB; ++i) {
+            const float2 a = upk2(acc4[i]);
+            r4[i] = a.x;
+            i4[i] = -a.y;
           }
           if (lanes >= n_lb) {
 #pragma unroll

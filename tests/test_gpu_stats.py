@@ -65,6 +65,19 @@ def test_stats_parity_odd_tone_count():
     assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0])
 
 
+def test_stats_parity_ragged_shape():
+    """M = 5 antennas (a partial 4-column group in K7c, a partial 16-column chunk in K8), K = 3 users, N = 302
+    tones (a partial 128-tone chunk and a partial 32-tone block), D = 37 lags, B = 40 bins (a masked second bin
+    group); run under every kernel policy by test_stats_parity_other_kernel_paths."""
+    cfg = dataclasses.replace(CONFIGS[2], M=5, K=3, N=302, b=40, stride=20)
+    x = workload.gen_pilots(cfg, 1)
+    y = workload.gen_instances(cfg, 1, x=x)
+    r_g, s2_g = _gpu_stats(y, x, 37, 40)
+    r_o, s2_o = oracle.estimate_stats(y, x, 37, 40)
+    assert abs(s2_g[0] / s2_o - 1) < 1e-4
+    assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0])
+
+
 def test_stats_skipped_and_empty_sets():
     cfg = CONFIGS[2]
     x = workload.gen_pilots(cfg, 0)
