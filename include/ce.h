@@ -51,7 +51,7 @@ typedef enum {
   CE_EINVAL = -1,  /* invalid argument: sizes, pointers, alignment, aliasing, sigma^2 */
   CE_ENOMEM = -2,  /* host or device allocation failed */
   CE_ECUDA = -3,   /* a CUDA runtime call failed (detail in ce_last_error) */
-  CE_ENOTPD = -4,  /* filter build: R_b + sigma^2 I not positive definite (Cholesky pivot <= 0 or NaN) */
+  CE_ENOTPD = -4,  /* filter build: R_b + sigma^2 I not positive definite (a pivot <= 0 or NaN) */
   CE_ESTATE = -5,  /* ce_estimate before a successful ce_build_filters */
   CE_ENODEV = -6   /* no CUDA device, or not compute capability 10.x */
 } ce_status;
@@ -88,11 +88,12 @@ typedef struct {
  * CE_ENODEV if no compute-capability-10 device is current; CE_ENOMEM on allocation failure. */
 int ce_init(const ce_params *p, ce_handle **out);
 
-/* K1 (Eq. 17; Cholesky as in the paper's cposv): per set,
- * A = R_b + sigma^2 I from the Toeplitz first column, FP64 complex Cholesky A = L L^H,
- * W = A^-1 R_b by forward/back substitution with b right-hand sides, rounded to complex64.
- * Enqueued on `stream`, then synchronises that stream once to read the positive-definite flag.
- * Returns CE_ENOTPD (handle stays unbuilt) if any pivot is <= 0 or not finite. */
+/* K1 (Eq. 17): per set, A = R_b + sigma^2 I from the Toeplitz first column (Hermitian
+ * Toeplitz), W = R_b A^-1 = I - sigma^2 A^-1 in FP64 by the Toeplitz structure in O(b^2): Levinson-Durbin for
+ * A^-1 e_0, then the Gohberg-Semencul (Trench) recurrence for every entry (the paper's own solver is a Cholesky,
+ * cposv); rounded to complex64.  Enqueued on `stream`, then synchronises that stream once to read
+ * the positive-definite flag.  Returns CE_ENOTPD (handle stays unbuilt) if a Levinson prediction-error power
+ * (a ratio of leading minors of A) is <= 0 or not finite. */
 int ce_build_filters(ce_handle *h, void *stream);
 
 /* K2/K3 hot path (a3-a5 of SURVEY.md §8(a)): for every instance t, window w and column (m,k)

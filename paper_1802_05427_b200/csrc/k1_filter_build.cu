@@ -2,19 +2,23 @@
 //
 //   W_b = R_b (R_b + sigma^2 I)^-1            PAPER.md:306-309 (Eq. 17), square case (reading A2)
 //
-// R_b is the b x b leading block of the Hermitian Toeplitz R_hh built from its first column
-// r[d] ("only depends on the difference"); with Toeplitz R_hh one W_b serves
-// every window.  As in the paper's detector (LAPACKE_cposv) the Hermitian PD
-// system is solved by Cholesky:  A = R_b + sigma^2 I = L L^H, then W = A^-1 R_b by forward
-// (L Z = R_b) and back (L^H W = Z) substitution for the b right-hand sides.  A and R_b commute,
-// so A^-1 R_b = R_b A^-1 = W.  FP64 is required: an FP32 build alone exceeds the 1e-4 budget
-// at the config-4 condition numbers (SURVEY.md §7 "Accuracy").
-//
-// Kernel 1 (one CTA per set): packed lower-triangular Cholesky, in shared memory when it fits
-//   (b <= 168), else in the global workspace; writes L (packed) to the workspace.
-// Kernel 2 (grid sets x ceil(b/8), one warp per right-hand side): loads packed L into shared
-//   memory, forward/back substitution, writes W (row-major) and W^T (for K2's coalesced loads)
-//   rounded to complex64.
+// R_b is the b x b leading block of the Hermitian Toeplitz R_hh built from its first column r[d] (PAPER.md:287,
+// "only depends on the difference"); with Toeplitz R_hh one W_b serves every window.  A = R_b + sigma^2 I is
+// Hermitian Toeplitz too, and R_b = A - sigma^2 I, so
+//   W_b = (A - sigma^2 I) A^-1 = I - sigma^2 A^-1.
+// The paper solves its Hermitian PD systems by Cholesky (LAPACKE_cposv), O(b^3); here the Toeplitz
+// structure gives A^-1 in O(b^2):
+//   K1a (one warp per set): Levinson-Durbin recursion for x = A^-1 e_0.  Order-k forward vector f_k (f_k[0] = 1,
+//       T_{k+1} f_k = eps_k e_0): eta = sum_{m<k} c[k-m] f_{k-1}[m], gamma = -eta / eps_{k-1},
+//       f_k[m] = f_{k-1}[m] + gamma conj(f_{k-1}[k-m]) (m = 0..k, f_{k-1}[k] = 0), eps_k = eps_{k-1} (1 - |gamma|^2);
+//       x = f_{b-1} / eps_{b-1}.  A is PD iff every eps_k > 0 (leading minors): the CE_ENOTPD flag.
+//   K1b (one thread per diagonal): Gohberg-Semencul / Trench.  With B = A^-1 and x its first column,
+//       B = (1/x_0) (L1 L1^H - L2 L2^H),  L1 lower-triangular Toeplitz with first column x, L2 with first column
+//       (0, conj(x_{b-1}), ..., conj(x_1)), so along every diagonal
+//       B[i+1][j+1] = B[i][j] + (x[i+1] conj(x[j+1]) - conj(x[b-1-i]) x[b-1-j]) / x_0,   B[0][j] = conj(x[j]);
+//       thread d walks the diagonal j - i = d and writes W = I - sigma^2 B (Hermitian) to both triangles of W and
+//       of W^T (K2's coalesced layout), rounded to complex64.
+// FP64 throughout: an FP32 build alone exceeds the 1e-4 budget at the config-4 condition numbers.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -23,80 +27,12 @@
 namespace ce {
 namespace {
 
-constexpr int K1_THREADS = 256;
-constexpr int K1S_WARPS = 8;
-constexpr size_t SMEM_LIMIT = 220 * 1024;
-
-__device__ __forceinline__ size_t pk(int i, int j) { return size_t(i) * (i + 1) / 2 + j; }  // i >= j
+constexpr int K1B_THREADS = 128;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ double2 cmul_conj_b(double2 a, double2 b) {  // a * conj(b)
-  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
-}
-
-// R_b[i][j] of the Hermitian Toeplitz block: r[i-j] for i >= j, conj(r[j-i]) otherwise.
-__device__ __forceinline__ double2 toeplitz(const double2 *r, int i, int j) {
-  if (i >= j) return r[i - j];
-  double2 v = r[j - i];
-  return make_double2(v.x, -v.y);
-}
-
-__global__ void __launch_bounds__(K1_THREADS) k1_cholesky(const double2 *__restrict__ d_r,
-                                                          const double *__restrict__ d_sigma2, int b,
-                                                          double2 *__restrict__ ws, int use_smem,
-                                                          int32_t *__restrict__ flag) {
-  extern __shared__ double2 sm[];
-  const int s = blockIdx.x;
-  const size_t packed = size_t(b) * (b + 1) / 2;
-  double2 *L = use_smem ? sm : ws + size_t(s) * packed;
-  const double2 *r = d_r + size_t(s) * b;
-  const double sigma2 = d_sigma2[s];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  __shared__ double s_inv;
-
-  // A = R_b + sigma^2 I, lower triangle, packed by rows
-  for (int i = warp; i < b; i += nwarp)
-    for (int j = lane; j <= i; j += 32) {
-      double2 v = toeplitz(r, i, j);
-      if (i == j) v.x += sigma2;
-      L[pk(i, j)] = v;
-    }
-  __syncthreads();
-
-  for (int k = 0; k < b; ++k) {
-    if (tid == 0) {
-      const double d = L[pk(k, k)].x;
-      const bool bad = !(d > 0.0) || !isfinite(d);
-      if (bad) atomicOr(flag, 1);
-      const double lkk = bad ? nan("") : sqrt(d);
-      L[pk(k, k)] = make_double2(lkk, 0.0);
-      s_inv = 1.0 / lkk;
-    }
-    __syncthreads();
-    const double inv = s_inv;
-    for (int i = k + 1 + tid; i < b; i += blockDim.x) {
-      double2 v = L[pk(i, k)];
-      L[pk(i, k)] = make_double2(v.x * inv, v.y * inv);
-    }
-    __syncthreads();
-    // trailing update of the lower triangle: L(i,j) -= L(i,k) conj(L(j,k)), k < j <= i
-    for (int i = k + 1 + warp; i < b; i += nwarp) {
-      const double2 lik = L[pk(i, k)];
-      for (int j = k + 1 + lane; j <= i; j += 32) {
-        const double2 p = cmul_conj_b(lik, L[pk(j, k)]);
-        double2 v = L[pk(i, j)];
-        L[pk(i, j)] = make_double2(v.x - p.x, v.y - p.y);
-      }
-    }
-    __syncthreads();
-  }
-  if (use_smem) {
-    double2 *out = ws + size_t(s) * packed;
-    for (size_t e = tid; e < packed; e += blockDim.x) out[e] = L[e];
-  }
-}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
 __device__ __forceinline__ double2 warp_sum(double2 v) {
 #pragma unroll
@@ -107,62 +43,93 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
   return v;
 }
 
-__global__ void __launch_bounds__(K1S_WARPS * 32) k1_solve(const double2 *__restrict__ d_r, int b,
-                                                           const double2 *__restrict__ ws, int l_in_smem,
-                                                           float2 *__restrict__ W, float2 *__restrict__ Wt) {
-  extern __shared__ double2 sm[];
-  const int s = blockIdx.x;
-  const size_t packed = size_t(b) * (b + 1) / 2;
-  const double2 *Lg = ws + size_t(s) * packed;
-  double2 *z_all = sm;                                  // [K1S_WARPS][b]
-  double2 *Ls = sm + size_t(K1S_WARPS) * b;             // packed L copy (if it fits)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (l_in_smem)
-    for (size_t e = tid; e < packed; e += blockDim.x) Ls[e] = Lg[e];
-  __syncthreads();
-  const double2 *L = l_in_smem ? Ls : Lg;
+// K1a: one warp per set.  c = first column of A (r[d], plus sigma^2 on d = 0); f in shared memory.
+// Writes x = A^-1 e_0 to ws[s][0..b-1].
+__global__ void __launch_bounds__(32) k1_levinson(const double2 *__restrict__ d_r, const double *__restrict__ d_sigma2,
+                                                  int b, double2 *__restrict__ ws, int in_smem, int32_t *__restrict__ flag) {
+  extern __shared__ double2 sm1[];
+  const int s = blockIdx.x, lane = threadIdx.x;
+  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][c: b][f: b]
+  double2 *c = in_smem ? sm1 : wss + b + 1;          // [b]
+  double2 *f = c + b;                                // [b]
   const double2 *r = d_r + size_t(s) * b;
-  const int j = blockIdx.y * K1S_WARPS + warp;          // right-hand side (column of R_b)
-  if (j >= b) return;
-  double2 *z = z_all + size_t(warp) * b;
-  for (int i = lane; i < b; i += 32) z[i] = toeplitz(r, i, j);
+  const double sigma2 = d_sigma2[s];
+  for (int m = lane; m < b; m += 32) {
+    double2 v = r[m];
+    if (m == 0) v = make_double2(v.x + sigma2, 0.0);   // A is Hermitian: c[0] real
+    c[m] = v;
+    f[m] = make_double2(m == 0 ? 1.0 : 0.0, 0.0);
+  }
   __syncwarp();
-  // forward: L Z = R_b[:, j]
-  for (int i = 0; i < b; ++i) {
+  double eps = c[0].x;
+  bool bad = !(eps > 0.0) || !isfinite(eps);
+  for (int k = 1; k < b && !bad; ++k) {
     double2 acc = make_double2(0.0, 0.0);
-    for (int k = lane; k < i; k += 32) {
-      const double2 p = cmul(L[pk(i, k)], z[k]);
+    for (int m = lane; m < k; m += 32) {             // eta = sum_{m<k} c[k-m] f[m]
+      const double2 p = cmul(c[k - m], f[m]);
       acc.x += p.x;
       acc.y += p.y;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const double inv = 1.0 / L[pk(i, i)].x;
-      z[i] = make_double2((z[i].x - acc.x) * inv, (z[i].y - acc.y) * inv);
+    const double2 eta = warp_sum(acc);
+    const double2 gamma = make_double2(-eta.x / eps, -eta.y / eps);
+    // in-place pair update (m, k - m), m = 0..k/2: f[m] += gamma conj(f[k-m]), f[k-m] += gamma conj(f[m])
+    for (int m = lane; 2 * m <= k; m += 32) {
+      const double2 fm = f[m], fk = f[k - m];
+      const double2 um = cmul(gamma, cconj(fk));
+      if (2 * m == k) {
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+      } else {
+        const double2 uk = cmul(gamma, cconj(fm));
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+        f[k - m] = make_double2(fk.x + uk.x, fk.y + uk.y);
+      }
     }
     __syncwarp();
+    eps *= 1.0 - (gamma.x * gamma.x + gamma.y * gamma.y);
+    bad = !(eps > 0.0) || !isfinite(eps);
   }
-  // back: L^H W = Z
-  for (int i = b - 1; i >= 0; --i) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k = i + 1 + lane; k < b; k += 32) {
-      const double2 p = cmul_conj_b(z[k], L[pk(k, i)]);  // conj(L(k,i)) * z[k]
-      acc.x += p.x;
-      acc.y += p.y;
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const double inv = 1.0 / L[pk(i, i)].x;
-      z[i] = make_double2((z[i].x - acc.x) * inv, (z[i].y - acc.y) * inv);
-    }
-    __syncwarp();
-  }
+  if (bad && lane == 0) atomicOr(flag, 1);
+  const double inv = bad ? nan("") : 1.0 / eps;
+  __syncwarp();
+  for (int m = lane; m < b; m += 32) wss[m] = make_double2(f[m].x * inv, f[m].y * inv);
+}
+
+// K1b: grid (sets, ceil(b / 128)); thread d walks the diagonal j - i = d of B = A^-1.
+__global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restrict__ d_sigma2, int b,
+                                                         const double2 *__restrict__ ws, int in_smem,
+                                                         float2 *__restrict__ W, float2 *__restrict__ Wt) {
+  extern __shared__ double2 sx[];                    // [b] x, when it fits
+  const int s = blockIdx.x;
+  const double2 *xg = ws + size_t(s) * (3 * size_t(b) + 1);
+  if (in_smem)
+    for (int m = threadIdx.x; m < b; m += blockDim.x) sx[m] = xg[m];
+  __syncthreads();
+  const double2 *xs = in_smem ? sx : xg;
+  const int d = blockIdx.y * blockDim.x + threadIdx.x;
+  if (d >= b) return;
+  const double sigma2 = d_sigma2[s];
+  const double ix0 = 1.0 / xs[0].x;
   float2 *Ws = W + size_t(s) * b * b;
   float2 *Wts = Wt + size_t(s) * b * b;
-  for (int i = lane; i < b; i += 32) {
-    const float2 v = make_float2(__double2float_rn(z[i].x), __double2float_rn(z[i].y));
-    Ws[size_t(i) * b + j] = v;   // W[i][j]
-    Wts[size_t(j) * b + i] = v;  // W^T[j][i]
+  double2 v = cconj(xs[d]);                          // B[0][d]
+  for (int i = 0; i + d < b; ++i) {
+    const int j = i + d;
+    // W = I - sigma^2 B: upper element (i, j) and, by Hermitian symmetry, lower element (j, i)
+    const double2 w = make_double2((i == j ? 1.0 : 0.0) - sigma2 * v.x, -sigma2 * v.y);
+    const float2 wu = make_float2(__double2float_rn(w.x), __double2float_rn(w.y));
+    const float2 wl = make_float2(wu.x, -wu.y);
+    Ws[size_t(i) * b + j] = wu;                      // W[i][j]
+    Wts[size_t(j) * b + i] = wu;                     // W^T[j][i] = W[i][j]
+    if (d != 0) {
+      Ws[size_t(j) * b + i] = wl;                    // W[j][i] = conj(W[i][j])
+      Wts[size_t(i) * b + j] = wl;                   // W^T[i][j] = W[j][i]
+    }
+    if (j + 1 < b) {                                 // B[i+1][j+1] = B[i][j] + (x[i+1] x*[j+1] - x*[b-1-i] x[b-1-j]) / x0
+      const double2 p = cmul(xs[i + 1], cconj(xs[j + 1]));
+      const double2 q = cmul(cconj(xs[b - 1 - i]), xs[b - 1 - j]);
+      v.x += (p.x - q.x) * ix0;
+      v.y += (p.y - q.y) * ix0;
+    }
   }
 }
 
@@ -172,24 +139,25 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
                                 double2 *d_ws, float2 *d_W, float2 *d_Wt, int32_t *d_flag, cudaStream_t stream,
                                 int64_t *launches) {
   (void)N;
-  const size_t packed_bytes = size_t(b) * (b + 1) / 2 * sizeof(double2);
-  const int chol_smem = packed_bytes <= SMEM_LIMIT;
   cudaError_t e;
-  if (chol_smem) {
-    e = cudaFuncSetAttribute(k1_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, int(packed_bytes));
+  // f and c in shared memory up to b = 6400, else in the set's workspace (ws: [n_sets][3b + 1] double2)
+  const int lev_in_smem = size_t(2) * b * sizeof(double2) <= 200 * 1024;
+  const size_t lev_smem = lev_in_smem ? size_t(2) * b * sizeof(double2) : 0;
+  if (lev_smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k1_levinson, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
     if (e != cudaSuccess) return e;
   }
-  k1_cholesky<<<n_sets, K1_THREADS, chol_smem ? packed_bytes : 0, stream>>>(d_r, d_sigma2, b, d_ws, chol_smem,
-                                                                              d_flag);
+  k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  const size_t z_bytes = size_t(K1S_WARPS) * b * sizeof(double2);
-  const int l_smem = z_bytes + packed_bytes <= SMEM_LIMIT;
-  const size_t solve_smem = z_bytes + (l_smem ? packed_bytes : 0);
-  e = cudaFuncSetAttribute(k1_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(solve_smem));
-  if (e != cudaSuccess) return e;
-  dim3 grid(n_sets, (b + K1S_WARPS - 1) / K1S_WARPS);
-  k1_solve<<<grid, K1S_WARPS * 32, solve_smem, stream>>>(d_r, b, d_ws, l_smem, d_W, d_Wt);
+  const int tr_in_smem = size_t(b) * sizeof(double2) <= 200 * 1024;
+  const size_t tr_smem = tr_in_smem ? size_t(b) * sizeof(double2) : 0;
+  if (tr_smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k1_trench, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tr_smem));
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(n_sets, (b + K1B_THREADS - 1) / K1B_THREADS);
+  k1_trench<<<grid, K1B_THREADS, tr_smem, stream>>>(d_sigma2, b, d_ws, tr_in_smem, d_W, d_Wt);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   return cudaSuccess;
