@@ -18,6 +18,7 @@
 //       B[i+1][j+1] = B[i][j] + (x[i+1] conj(x[j+1]) - conj(x[b-1-i]) x[b-1-j]) / x_0,   B[0][j] = conj(x[j]);
 //       thread d walks the diagonal j - i = d and writes W = I - sigma^2 B (Hermitian) to both triangles of W and
 //       of W^T (K2's coalesced layout), rounded to complex64.
+//   K1r between them: one step of iterative refinement of x (Levinson-Durbin is only weakly stable).
 // FP64 throughout: an FP32 build alone exceeds the 1e-4 budget at the config-4 condition numbers.
 #include <cuda_runtime.h>
 #include <math.h>
@@ -94,6 +95,78 @@ __global__ void __launch_bounds__(32) k1_levinson(const double2 *__restrict__ d_
   for (int m = lane; m < b; m += 32) wss[m] = make_double2(f[m].x * inv, f[m].y * inv);
 }
 
+// K1r: one step of iterative refinement of x (one CTA per set).  Levinson-Durbin is only weakly stable: at
+// condition numbers ~1e8 its x is off by ~1e-6 relative (W by ~5e-6) where a backward-stable solve gives ~1e-8.
+// With the residual res = e_0 - A x (exact Toeplitz products in FP64) and the Gohberg-Semencul form of the
+// current inverse, x += (1/x_0) (L1 L1^H res - L2 L2^H res) brings x to the backward-stable level (4 triangular
+// Toeplitz products and one Toeplitz product, O(b^2), one thread per output index).
+constexpr int K1R_THREADS = 256;
+__global__ void __launch_bounds__(K1R_THREADS) k1_refine(const double2 *__restrict__ d_r,
+                                                         const double *__restrict__ d_sigma2, int b,
+                                                         double2 *__restrict__ ws) {
+  extern __shared__ double2 sr[];
+  double2 *c = sr, *x = sr + b, *res = sr + 2 * b, *u = sr + 3 * b, *u2 = sr + 4 * b;
+  const int s = blockIdx.x, tid = threadIdx.x;
+  double2 *xg = ws + size_t(s) * (3 * size_t(b) + 1);
+  const double2 *r = d_r + size_t(s) * b;
+  for (int m = tid; m < b; m += blockDim.x) {
+    double2 v = r[m];
+    if (m == 0) v = make_double2(v.x + d_sigma2[s], 0.0);
+    c[m] = v;
+    x[m] = xg[m];
+  }
+  __syncthreads();
+  // res[i] = delta_i0 - sum_j A[i][j] x[j],  A[i][j] = c[i-j] (i >= j), conj(c[j-i]) (i < j)
+  for (int i = tid; i < b; i += blockDim.x) {
+    double2 acc = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    for (int j = 0; j <= i; ++j) {
+      const double2 p = cmul(c[i - j], x[j]);
+      acc.x -= p.x;
+      acc.y -= p.y;
+    }
+    for (int j = i + 1; j < b; ++j) {
+      const double2 p = cmul(cconj(c[j - i]), x[j]);
+      acc.x -= p.x;
+      acc.y -= p.y;
+    }
+    res[i] = acc;
+  }
+  __syncthreads();
+  // u = L1^H res: u[k] = sum_{i>=k} conj(x[i-k]) res[i];  u2 = L2^H res: u2[k] = sum_{i>k} x[b-(i-k)] res[i]
+  for (int k = tid; k < b; k += blockDim.x) {
+    double2 a = make_double2(0.0, 0.0), a2 = make_double2(0.0, 0.0);
+    for (int i = k; i < b; ++i) {
+      const double2 p = cmul(cconj(x[i - k]), res[i]);
+      a.x += p.x;
+      a.y += p.y;
+      if (i > k) {
+        const double2 q = cmul(x[b - (i - k)], res[i]);
+        a2.x += q.x;
+        a2.y += q.y;
+      }
+    }
+    u[k] = a;
+    u2[k] = a2;
+  }
+  __syncthreads();
+  // delta[i] = (sum_{k<=i} x[i-k] u[k] - sum_{k<i} conj(x[b-i+k]) u2[k]) / x_0
+  const double ix0 = 1.0 / x[0].x;
+  for (int i = tid; i < b; i += blockDim.x) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int k = 0; k <= i; ++k) {
+      const double2 p = cmul(x[i - k], u[k]);
+      a.x += p.x;
+      a.y += p.y;
+      if (k < i) {
+        const double2 q = cmul(cconj(x[b - i + k]), u2[k]);
+        a.x -= q.x;
+        a.y -= q.y;
+      }
+    }
+    xg[i] = make_double2(x[i].x + a.x * ix0, x[i].y + a.y * ix0);
+  }
+}
+
 // K1b: grid (sets, ceil(b / 128)); thread d walks the diagonal j - i = d of B = A^-1.
 __global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restrict__ d_sigma2, int b,
                                                          const double2 *__restrict__ ws, int in_smem,
@@ -150,6 +223,17 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
+  // one refinement step of x when its five work vectors fit in shared memory (b <= 2560)
+  const size_t ref_smem = size_t(5) * b * sizeof(double2);
+  if (ref_smem <= 200 * 1024) {
+    if (ref_smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(k1_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ref_smem));
+      if (e != cudaSuccess) return e;
+    }
+    k1_refine<<<n_sets, K1R_THREADS, ref_smem, stream>>>(d_r, d_sigma2, b, d_ws);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++*launches;
+  }
   const int tr_in_smem = size_t(b) * sizeof(double2) <= 200 * 1024;
   const size_t tr_smem = tr_in_smem ? size_t(b) * sizeof(double2) : 0;
   if (tr_smem > 48 * 1024) {

@@ -175,6 +175,26 @@ def test_filters_match_oracle():
         est.close()
 
 
+@pytest.mark.parametrize("b,sigma2", [(100, 1e-4), (300, 1e-6), (1200, 1e-3)])
+def test_filters_ill_conditioned_and_full_band(b, sigma2):
+    """K1's O(b^2) Toeplitz build (Levinson-Durbin + Trench) on badly conditioned designs: a sparse 8-tap delay
+    profile (rank-deficient R_b) with SNR_fixed = 40-60 dB (condition numbers ~1e5-1e8, PAPER.md:306's fixed
+    design regime) and the full-band b = N = 1200 case; same complex64-rounding bar as the matched builds."""
+    ce = _ce()
+    N = 1200
+    taps = np.array([0.0, 3.0, 7.5, 12.0, 20.0, 33.0, 41.5, 57.0])      # delays in samples of Nfft = 2048
+    p = np.exp(-np.arange(8) / 3.0)
+    p /= p.sum()
+    d = np.arange(N)
+    r = (p[None, :] * np.exp(-2j * np.pi * d[:, None] * taps[None, :] / 2048)).sum(axis=1)[None, :]
+    est = ce.ChannelEstimator(N, b, b, r, [sigma2]).build()
+    W = est.filters()[0]
+    est.close()
+    ref = oracle.block_filter(r[0], sigma2, b)
+    rel = np.linalg.norm(W - ref) / np.linalg.norm(ref)
+    assert rel < 2e-7, rel
+
+
 def test_not_positive_definite_and_state():
     ce = _ce()
     N = 16
