@@ -13,7 +13,8 @@
 // FP64 accumulator (K7's layout: K7 adds the noise floor and the column count, K7b normalises).
 //
 // Roles (persistent CTAs, 448 threads):
-//   warp 12   : TMA of the raw y boxes [16 columns][128 tones] of tiles i and j into a 2-deep raw ring
+//   warp 12   : TMA of the raw y boxes [16 antennas of one user][128 tones] of tiles i and j (4-D map, so a
+//               chunk's columns share one user and one LS factor per tone) into a 2-deep raw ring
 //   warps 0-7 : transform -- per unit the LS factors conj(x)/|x|^2 of tiles i and j for every user; per
 //               16-column chunk the LS values transposed into the K-major A tile (row n: the chunk's 16 columns)
 //               and B tile (rows 2n', 2n'+1), bf16 hi/lo, SWIZZLE_64B, 2-deep A/B ring
@@ -55,13 +56,14 @@ struct K8Params {
   const int32_t *soi;
   const float2 *x;
   double *acc;                            // [n_sets][2D + 2]
-  int T, MK, K, N, D, n_sets;
-  int n_pairs, n_cc, cc_cols, n_units;    // units = T x n_cc x n_pairs (pair fastest)
+  int T, M, K, N, D, n_sets;
+  int nmc;                                // 16-antenna chunks per user: chunk q of an instance = (k = q / nmc, m0 = 16 (q % nmc))
+  int n_pairs, n_cc, cq, n_units;         // units = T x n_cc x n_pairs (pair fastest), cq chunks per unit
   short2 pairs[MAXP8];                    // (i, j) tone tiles
 };
 
 struct Unit8 {
-  int t, c0, c1, i, j;
+  int t, q0, q1, i, j;
 };
 
 __device__ __forceinline__ Unit8 decode8(const K8Params &p, int u) {
@@ -70,8 +72,8 @@ __device__ __forceinline__ Unit8 decode8(const K8Params &p, int u) {
   const int rest = u / p.n_pairs;
   const int cc = rest % p.n_cc;
   un.t = rest / p.n_cc;
-  un.c0 = cc * p.cc_cols;
-  un.c1 = min(p.MK, un.c0 + p.cc_cols);
+  un.q0 = cc * p.cq;
+  un.q1 = min(p.K * p.nmc, un.q0 + p.cq);
   un.i = p.pairs[pr].x;
   un.j = p.pairs[pr].y;
   return un;
@@ -147,13 +149,14 @@ __global__ void __launch_bounds__(K8_THREADS, 1)
       int it = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit8 un = decode8(p, u);
-        for (int c = un.c0; c < un.c1; c += CC8, ++it) {
+        for (int q = un.q0; q < un.q1; ++q, ++it) {
           const int s = it % S_RAW8;
           mbar_wait(&raw_empty[s], ((it / S_RAW8) & 1) ^ 1);
           mbar_arrive_expect_tx(&raw_full[s], RAW8);
-          const int row = un.t * p.MK + c;
-          tma_load_2d(raw + s * RAW8, &tmy, 2 * TT * un.i, row, &raw_full[s]);
-          tma_load_2d(raw + s * RAW8 + RAW_TILE, &tmy, 2 * TT * un.j, row, &raw_full[s]);
+          // 16 antennas m0.. of user k (rows beyond M are zero-filled: zero LS values)
+          const int k = q / p.nmc, m0 = CC8 * (q % p.nmc);
+          tma_load_4d(raw + s * RAW8, &tmy, 2 * TT * un.i, k, m0, un.t, &raw_full[s]);
+          tma_load_4d(raw + s * RAW8 + RAW_TILE, &tmy, 2 * TT * un.j, k, m0, un.t, &raw_full[s]);
         }
       }
     }
@@ -178,8 +181,11 @@ __global__ void __launch_bounds__(K8_THREADS, 1)
         fac[e] = f;
       }
       named_bar_sync(1, NTR8);
-      for (int c = un.c0; c < un.c1; c += CC8, ++it) {
+      for (int q = un.q0; q < un.q1; ++q, ++it) {
         const int sr = it % S_RAW8, sa = it % S_AB8;
+        // every column of the chunk belongs to user k: one pair of LS factors per thread and chunk
+        const int k = q / p.nmc;
+        const float2 fi = fac[k * TT + n], fj = fac[(p.K + k) * TT + n];
         mbar_wait(&raw_full[sr], (it / S_RAW8) & 1);
         const float2 *ri = reinterpret_cast<const float2 *>(raw + sr * RAW8);
         const float2 *rj = reinterpret_cast<const float2 *>(raw + sr * RAW8 + RAW_TILE);
@@ -187,13 +193,10 @@ __global__ void __launch_bounds__(K8_THREADS, 1)
         uint32_t ah[8], al[8], b0h[8], b0l[8], b1h[8], b1l[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int cl = 8 * hc + e, col = c + cl;
-          const int k = col % p.K;
+          const int cl = 8 * hc + e;
           const float2 yi = ri[cl * TT + n], yj = rj[cl * TT + n];
-          const float2 fi = fac[k * TT + n], fj = fac[(p.K + k) * TT + n];
-          float2 a = make_float2(yi.x * fi.x - yi.y * fi.y, yi.x * fi.y + yi.y * fi.x);
-          float2 b = make_float2(yj.x * fj.x - yj.y * fj.y, yj.x * fj.y + yj.y * fj.x);
-          if (col >= un.c1) a = b = make_float2(0.f, 0.f);        // past the unit's columns
+          const float2 a = make_float2(yi.x * fi.x - yi.y * fi.y, yi.x * fi.y + yi.y * fi.x);
+          const float2 b = make_float2(yj.x * fj.x - yj.y * fj.y, yj.x * fj.y + yj.y * fj.x);
           split2(a.x, a.y, ah[e], al[e]);
           split2(b.x, b.y, b0h[e], b0l[e]);
           split2(b.y, -b.x, b1h[e], b1l[e]);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(K8_THREADS, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * 256);
         bool first = true;
-        for (int c = un.c0; c < un.c1; c += CC8, ++it) {
+        for (int q = un.q0; q < un.q1; ++q, ++it) {
           const int s = it % S_AB8;
           mbar_wait(&a_full[s], (it / S_AB8) & 1);
           tc_fence_after();
@@ -334,7 +337,8 @@ cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, 
   p.x = x;
   p.acc = acc;
   p.T = T;
-  p.MK = M * K;
+  p.M = M;
+  p.nmc = (M + CC8 - 1) / CC8;
   p.K = K;
   p.N = N;
   p.D = D;
@@ -347,17 +351,19 @@ cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, 
   p.n_pairs = np;
   // columns per unit: about one unit per SM (each unit pays a factor table and 2D atomics), whole 16-column
   // chunks, at most one instance
-  const long long work = (long long)T * np * p.MK;
+  // chunks per unit: about one unit per SM (each unit pays a factor table and 2D atomics), at most one instance
+  const int nq = K * p.nmc;                        // 16-column chunks per instance
+  const long long work = (long long)T * np * nq;
   static const int env_upsm = getenv("CE_K8_UPSM") ? atoi(getenv("CE_K8_UPSM")) : 1;   // experiments
-  long long cc = work / (std::max(1, env_upsm) * (long long)nsm);
-  cc = std::max<long long>(CC8, std::min<long long>(cc, 4096)) / CC8 * CC8;
-  p.cc_cols = int(std::min<long long>(cc, ((long long)p.MK + CC8 - 1) / CC8 * CC8));
-  p.n_cc = (p.MK + p.cc_cols - 1) / p.cc_cols;
+  long long cq = work / (std::max(1, env_upsm) * (long long)nsm);
+  cq = std::max<long long>(1, std::min<long long>(cq, std::min(256, nq)));
+  p.cq = int(cq);
+  p.n_cc = (nq + p.cq - 1) / p.cq;
   const long long units = (long long)T * p.n_cc * np;
   if (units > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   p.n_units = int(units);
   CUtensorMap tmy;
-  if (!make_map(&tmy, y, N, (long long)T * p.MK, CC8, 2 * TT)) return cudaErrorInvalidValue;
+  if (!make_map_kmajor(&tmy, y, N, K, M, T, CC8, 2 * TT)) return cudaErrorInvalidValue;
   k8_gram<<<unsigned(std::min<long long>(units, nsm)), K8_THREADS, K8_SMEM, stream>>>(tmy, p);
   return cudaGetLastError();
 }

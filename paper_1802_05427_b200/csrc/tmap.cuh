@@ -37,6 +37,21 @@ bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_ro
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// y [T][M][K][2N floats] as a 4-D tensor (2N, K, M, T): box {box_floats, 1, box_rows, 1} = box_rows antennas of
+// one user (K8: a chunk's columns share their LS factors); antennas beyond M are zero-filled.
+bool make_map_kmajor(CUtensorMap *m, const void *ptr, int N, int K, int M, int T, int box_rows, int box_floats) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {cuuint64_t(2) * N, cuuint64_t(K), cuuint64_t(M), cuuint64_t(T)};
+  const cuuint64_t row = cuuint64_t(2) * N * 4;
+  cuuint64_t strides[3] = {row, row * K, row * K * M};
+  cuuint32_t box[4] = {cuuint32_t(box_floats), 1, cuuint32_t(box_rows), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void *>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // [rows][2N] float tensor, box [box_rows][box_floats], SWIZZLE_128B (box_floats * 4 == 128): store maps.
 bool make_map_sw128(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows) {
   EncodeTiledFn fn = encode_fn();
