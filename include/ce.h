@@ -211,7 +211,7 @@ int ce_comb_free(ce_comb_handle *h);
 int ce_stats_workspace_bytes(int32_t n_sets, int32_t D, int64_t *out);
 /* Device pointers, asynchronous on `stream` (K7a accumulate + K7b normalise; from 16384 columns T*M*K up, with
  * K <= 24, D <= 512, N even and d_y 16-byte aligned, the lag sums run on the tensor cores as a banded Gram
- * matrix (K8, BF16x3) and K7a adds only the noise floor -- same results within the 1e-4 parity bar):
+ * matrix (K8, BF16x3) and the noise floor is streamed by K7c -- same results within the 1e-4 parity bar):
  *   d_y [T][M][K][N], d_x [T][K][N] complex64 (8-byte aligned); d_set_of_instance int32 [T] or NULL (all
  *   set 0; instances with an out-of-range set are skipped); d_r out: complex128 [n_sets][D] interleaved;
  *   d_sigma2 out: float64 [n_sets]; d_work: ce_stats_workspace_bytes bytes.  A set with no instance gets
