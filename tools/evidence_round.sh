@@ -14,3 +14,5 @@ bash tools/profile_round.sh ${TAG}
 # statistics path (NEXT-3): bench lines for configs 3-5 and the config-4 launch list (K8 / K7c / K7b shares)
 for c in 3 4 5; do timeout 300 python bench.py --stats --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/stats_c${c}_${TAG}.json 2> gpurun_out/stats_c${c}_${TAG}.err; echo "stats c$c exit $?"; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file gpurun_out/launches_stats_c4_${TAG}.csv python bench.py --stats --config 4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_stats_${TAG}.log 2>&1; echo "stats launch list rc $?"
+# NEXT-row kernels: one --set full capture each (K8, K7c, K7a, K6 12W) + summary
+bash tools/profile_next.sh ${TAG}
