@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_accumulate(const float2 *__rest
 // K7c -- the noise window on its own, streamed: one CTA per (instance t, user k, range of antennas m), so one x
 // row (the LS factors conj(x)/|x|^2) serves all its columns c = (m, k).  Each warp owns every 8th group of 4
 // columns of the range and streams the group's y rows in 128-tone chunks into its own 2-deep ring by 1-D bulk
-// copies (no CTA barrier in the loop), converts the chunk to LS values in place, then runs a per-32-tone Horner
+// copies (no CTA barrier in the loop), converts the chunk to LS values in place, then runs a per-block (64-tone) Horner
 // recursion: lane l works on column l / 8 of the group and on NB bins (l % 8) + 8 j, so every broadcast 2-tone
 // shared-memory read (a quarter-warp per column) feeds 4 NB FMAs -- broadcast 16-byte reads cost one wavefront
 // per quarter-warp, so one bin per lane left the kernel bound by shared-memory wavefronts.  Bins beyond 8 NB run
@@ -270,6 +270,10 @@ constexpr int NZ_CPW = 4;      // columns per warp job
 constexpr int NZ_R = 2;        // chunks in flight per warp
 constexpr int NZ_WARPS = 8;
 constexpr int NZ_NB = 4;       // bins per lane per pass (8 NB bins per pass)
+#ifndef K7C_BLK
+#define K7C_BLK 64
+#endif
+constexpr int NZ_BLK = K7C_BLK; // tones per Horner block (the per-block rotation and sum are the overhead)
 
 __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                           int M, int K, int N, const int32_t *__restrict__ soi,
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restri
         const float2 w2 = cmulf(w1[g], w1[g]);
         w2ab[g] = pk2(w2.x, w2.y);
         w2ba[g] = pk2(-w2.y, w2.x);
-        w32[g] = twiddle(int((32LL * kap[g]) % N), N);
+        w32[g] = twiddle(int((static_cast<long long>(NZ_BLK) * kap[g]) % N), N);
         xr_[g] = xi_[g] = 0.f;
       }
     }
@@ -364,26 +368,26 @@ __global__ void __launch_bounds__(NZ_WARPS * 32) k7_noise(const float2 *__restri
       *reinterpret_cast<float4 *>(rb + e) = v;
     }
     __syncwarp();
-    const int nb = (len + 31) / 32;
+    const int nb = (len + NZ_BLK - 1) / NZ_BLK;   // zero-padded to whole blocks by the conversion
     const float2 *rc = rb + ci * NZ_CH;
     // rot = e^{j 2 pi n kap / N} at the block start n: 1 at the column start, advanced by e^{j 2 pi 32 kap / N} per
-    // block and re-seeded exactly every 8 chunks (at most 32 FP32 rotation steps between exact values)
+    // block and re-seeded exactly every 8 chunks (at most 8 CH / NZ_BLK FP32 rotation steps between exact values)
     if (ch % 8 == 0) {
 #pragma unroll
       for (int g = 0; g < NB; ++g)
         rot[g] = ch == 0 ? make_float2(1.f, 0.f) : twiddle(int((static_cast<long long>(n0) * kap[g]) % N), N);
     }
     for (int bb = 0; bb < nb; ++bb) {
-      const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(rc + bb * 32);   // (tone 2q, tone 2q+1)
+      const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(rc + bb * NZ_BLK);   // (tone 2q, tone 2q+1)
       uint64_t ev[NB], od[NB];                       // even / odd tone chains, packed (re, im)
-      ulonglong2 v = vp[15];                         // tones 30 and 31
+      ulonglong2 v = vp[NZ_BLK / 2 - 1];             // the block's last two tones
 #pragma unroll
       for (int g = 0; g < NB; ++g) {
         ev[g] = v.x;
         od[g] = v.y;
       }
 #pragma unroll
-      for (int q = 14; q >= 0; --q) {
+      for (int q = NZ_BLK / 2 - 2; q >= 0; --q) {
         v = vp[q];
 #pragma unroll
         for (int g = 0; g < NB; ++g) {
