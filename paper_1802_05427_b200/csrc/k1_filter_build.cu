@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(32) k1_levinson(const double2 *__restrict__ d_
 // With the residual res = e_0 - A x (exact Toeplitz products in FP64) and the Gohberg-Semencul form of the
 // current inverse, x += (1/x_0) (L1 L1^H res - L2 L2^H res) brings x to the backward-stable level (4 triangular
 // Toeplitz products and one Toeplitz product, O(b^2), one thread per output index).
-constexpr int K1R_THREADS = 256;
+constexpr int K1R_THREADS = 1024;
 __global__ void __launch_bounds__(K1R_THREADS) k1_refine(const double2 *__restrict__ d_r,
                                                          const double *__restrict__ d_sigma2, int b,
                                                          double2 *__restrict__ ws) {
@@ -167,6 +167,69 @@ __global__ void __launch_bounds__(K1R_THREADS) k1_refine(const double2 *__restri
   }
 }
 
+// K1a for large b (one CTA per set): the same recursion with the dot product spread over the CTA -- per step a
+// warp reduction, one barrier, every thread summing the per-warp partials in the same order (identical gamma
+// and eps everywhere), the pair update, and a second barrier.
+constexpr int K1L_THREADS = 512;
+__global__ void __launch_bounds__(K1L_THREADS) k1_levinson_cta(const double2 *__restrict__ d_r,
+                                                               const double *__restrict__ d_sigma2, int b,
+                                                               double2 *__restrict__ ws, int in_smem,
+                                                               int32_t *__restrict__ flag) {
+  extern __shared__ double2 sm1[];
+  __shared__ double2 part[2][K1L_THREADS / 32];
+  const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][c: b][f: b]
+  double2 *c = in_smem ? sm1 : wss + b + 1;
+  double2 *f = c + b;
+  const double2 *r = d_r + size_t(s) * b;
+  const double sigma2 = d_sigma2[s];
+  for (int m = tid; m < b; m += blockDim.x) {
+    double2 v = r[m];
+    if (m == 0) v = make_double2(v.x + sigma2, 0.0);
+    c[m] = v;
+    f[m] = make_double2(m == 0 ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  double eps = c[0].x;
+  bool bad = !(eps > 0.0) || !isfinite(eps);
+  for (int k = 1; k < b && !bad; ++k) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int m = tid; m < k; m += blockDim.x) {
+      const double2 p = cmul(c[k - m], f[m]);
+      acc.x += p.x;
+      acc.y += p.y;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[k & 1][warp] = acc;
+    __syncthreads();
+    double2 eta = make_double2(0.0, 0.0);
+    for (int w = 0; w < nw; ++w) {
+      eta.x += part[k & 1][w].x;
+      eta.y += part[k & 1][w].y;
+    }
+    const double2 gamma = make_double2(-eta.x / eps, -eta.y / eps);
+    for (int m = tid; 2 * m <= k; m += blockDim.x) {
+      const double2 fm = f[m], fk = f[k - m];
+      const double2 um = cmul(gamma, cconj(fk));
+      if (2 * m == k) {
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+      } else {
+        const double2 uk = cmul(gamma, cconj(fm));
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+        f[k - m] = make_double2(fk.x + uk.x, fk.y + uk.y);
+      }
+    }
+    eps *= 1.0 - (gamma.x * gamma.x + gamma.y * gamma.y);
+    bad = !(eps > 0.0) || !isfinite(eps);
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(flag, 1);
+  const double inv = bad ? nan("") : 1.0 / eps;
+  __syncthreads();
+  for (int m = tid; m < b; m += blockDim.x) wss[m] = make_double2(f[m].x * inv, f[m].y * inv);
+}
+
 // K1b: grid (sets, ceil(b / 128)); thread d walks the diagonal j - i = d of B = A^-1.
 __global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restrict__ d_sigma2, int b,
                                                          const double2 *__restrict__ ws, int in_smem,
@@ -216,11 +279,18 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   // f and c in shared memory up to b = 6400, else in the set's workspace (ws: [n_sets][3b + 1] double2)
   const int lev_in_smem = size_t(2) * b * sizeof(double2) <= 200 * 1024;
   const size_t lev_smem = lev_in_smem ? size_t(2) * b * sizeof(double2) : 0;
+  // one warp per set up to b = 256 (no barriers), a 512-thread CTA per set above (the length-k dot product of every
+  // step dominates: config 6, b = 1200, 1.74 ms with one warp)
+  const bool lev_cta = b > 256;
   if (lev_smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k1_levinson, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
+    e = cudaFuncSetAttribute(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
     if (e != cudaSuccess) return e;
   }
-  k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
+  if (lev_cta)
+    k1_levinson_cta<<<n_sets, K1L_THREADS, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
+  else
+    k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   // one refinement step of x when its five work vectors fit in shared memory (b <= 2560)
