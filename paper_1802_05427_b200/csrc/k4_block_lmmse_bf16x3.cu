@@ -98,6 +98,7 @@ struct K4Params {
   int tma_store;             // 1: interior 32-float column blocks leave through SW128 staging + TMA stores
   int tma_last;              // 1: the same for each CTA's last tile, staged in the then idle A/B ring
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
+  int l2_hint;               // bit 0: y loads evict_first; bit 1: h TMA stores evict_first (one-wave launches)
   Window geo_s[MAXW_PARAM];
 };
 
@@ -186,7 +187,11 @@ __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32);
+      if (p.l2_hint & 2)
+        tma_store_2d_hint(tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32,
+                          l2_evict_first_policy());
+      else
+        tma_store_2d(tmh, stg, 2 * ti.o - ti.off + 32 * cb, ti.t * p.cols + ti.ct * TM + q * 32);
       bulk_commit();
     }
     return;
@@ -327,7 +332,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           else if (it < 24) K4TR(8 + it);
 #endif
           const int f0 = 2 * (ti.a + kc * CK);        // first float of the chunk in the row
-          tma_load_2d(raw + s * RAW_STAGE, &tmy, f0, row0, &raw_full[s]);
+          if (p.l2_hint & 1)
+            tma_load_2d_hint(raw + s * RAW_STAGE, &tmy, f0, row0, &raw_full[s], l2_evict_first_policy());
+          else
+            tma_load_2d(raw + s * RAW_STAGE, &tmy, f0, row0, &raw_full[s]);
           tma_load_2d(raw + s * RAW_STAGE + RAWY, &tmx, f0, ti.t * K0, &raw_full[s]);
         }
       }
@@ -635,6 +643,13 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
     return cudaErrorInvalidValue;
   p.s_raw = p.tma_store ? S_RAW_MAX - 1 : S_RAW_MAX;
+  // y loads marked evict_first when every y element is read once and in one wave (tiles <= SMs, disjoint window
+  // inputs): measured -1.6% on config 3 (10.66 -> 10.48 us, same box); with overlapping windows or several tiles
+  // per SM the re-reads need y in L2 (configs 4-5 lost 8-10% with it).  Evict-first h stores measured no gain.
+  bool disjoint = a.geo_host != nullptr;
+  for (int w = 0; disjoint && w + 1 < a.n_win; ++w) disjoint = a.geo_host[w + 1].a >= a.geo_host[w].a + a.b;
+  static const int env_hint = getenv("CE_K4_L2HINT") ? atoi(getenv("CE_K4_L2HINT")) : -1;   // experiments
+  p.l2_hint = env_hint >= 0 ? env_hint : (tiles <= (long long)di->num_sms && disjoint ? 1 : 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
   cfg.blockDim = dim3(K4_THREADS);
