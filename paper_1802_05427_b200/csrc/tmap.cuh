@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 namespace ce {
 namespace {
 
@@ -25,6 +27,16 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// L2 promotion of the TMA load maps: 64 B measured best for K4 (config 3 10.48 -> 10.31-10.33 us same box, two
+// repetitions; configs 4-6 and the statistics kernels equal; 256 B was 2% slower).  CE_TMA_L2PROMO (experiments):
+// 0 none, 1 64B (default), 2 128B, 3 256B.
+CUtensorMapL2promotion load_promotion() {
+  static const int v = getenv("CE_TMA_L2PROMO") ? atoi(getenv("CE_TMA_L2PROMO")) : 1;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
 bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows, int box_floats = 32) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
@@ -33,7 +45,7 @@ bool make_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_ro
   cuuint32_t box[2] = {cuuint32_t(box_floats), cuuint32_t(box_rows)};   // 16 complex per box row by default
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, load_promotion(),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
