@@ -348,7 +348,7 @@ int ce_build_filters(ce_handle *h, void *stream) {
           "ce_build_filters: flag copy");
   CE_CUDA(cudaStreamSynchronize(st), "ce_build_filters: synchronize");
   if (*h->h_flag != 0)
-    return fail(CE_ENOTPD, "ce_build_filters: Cholesky pivot <= 0 or not finite (R_b + sigma^2 I not PD)");
+    return fail(CE_ENOTPD, "ce_build_filters: a Levinson prediction-error power <= 0 or not finite (R_b + sigma^2 I not PD)");
   h->built = true;
   return CE_OK;
 }
