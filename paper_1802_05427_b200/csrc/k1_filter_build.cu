@@ -23,6 +23,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "ce_internal.h"
 
 namespace ce {
@@ -230,6 +233,75 @@ __global__ void __launch_bounds__(K1L_THREADS) k1_levinson_cta(const double2 *__
   for (int m = tid; m < b; m += blockDim.x) wss[m] = make_double2(f[m].x * inv, f[m].y * inv);
 }
 
+// K1a' (Schur form, default): the same reflection coefficients without a per-step reduction.  With the residuals
+// of the forward and backward vectors, e_k[i] = (A [f_k; 0])[i] and r_k[i] = (A [b_k; 0])[i] (b_k = J conj(f_k)),
+// gamma_{k+1} = -e_k[k+1] / r_k[k] and, by the Toeplitz shift invariance, for i > k
+//   e_{k+1}[i] = e_k[i] + gamma r_k[i-1],   r_{k+1}[i] = r_k[i-1] + conj(gamma) e_k[i],
+// kept in place as R_k[j] = r_k[j + k] (thread j owns the pair (e[j+k+1], R[j])); f is updated by the same pair rule
+// as in K1a.  One barrier per step; the next step's two pivots go to a ping-pong slot.  e_0 = r_0 = c.
+__global__ void __launch_bounds__(K1L_THREADS) k1_schur(const double2 *__restrict__ d_r,
+                                                        const double *__restrict__ d_sigma2, int b,
+                                                        double2 *__restrict__ ws, int in_smem,
+                                                        int32_t *__restrict__ flag) {
+  extern __shared__ double2 sm1[];
+  __shared__ double2 piv[2][2];                      // [step parity][e_k[k+1], R_k[0]]
+  const int s = blockIdx.x, tid = threadIdx.x;
+  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][e: b][R: b] (f in x's slot when not in smem)
+  double2 *e = in_smem ? sm1 : wss + b + 1;
+  double2 *R = e + b;
+  double2 *f = in_smem ? sm1 + 2 * b : wss;
+  const double2 *r = d_r + size_t(s) * b;
+  const double sigma2 = d_sigma2[s];
+  for (int m = tid; m < b; m += blockDim.x) {
+    double2 v = r[m];
+    if (m == 0) v = make_double2(v.x + sigma2, 0.0);
+    e[m] = v;
+    R[m] = v;
+    f[m] = make_double2(m == 0 ? 1.0 : 0.0, 0.0);
+    if (m == 0) piv[0][1] = v;
+    if (m == 1) piv[0][0] = v;
+  }
+  __syncthreads();
+  double eps = piv[0][1].x;
+  bool bad = !(eps > 0.0) || !isfinite(eps);
+  for (int k = 0; k + 1 < b && !bad; ++k) {
+    const double2 ek = piv[k & 1][0], r0 = piv[k & 1][1];
+    const double den = r0.x * r0.x + r0.y * r0.y;
+    const double2 gamma = make_double2(-(ek.x * r0.x + ek.y * r0.y) / den, -(ek.y * r0.x - ek.x * r0.y) / den);
+    const double2 gc = cconj(gamma);
+    for (int j = tid; j < b - 1 - k; j += blockDim.x) {
+      const double2 eo = e[j + k + 1], ro = R[j];
+      const double2 p = cmul(gamma, ro), q = cmul(gc, eo);
+      const double2 en = make_double2(eo.x + p.x, eo.y + p.y), rn = make_double2(ro.x + q.x, ro.y + q.y);
+      e[j + k + 1] = en;
+      R[j] = rn;
+      if (j == 0) piv[(k + 1) & 1][1] = rn;            // R_{k+1}[0] = eps_{k+1}
+      if (j == 1) piv[(k + 1) & 1][0] = en;            // e_{k+1}[k+2]
+    }
+    for (int m = tid; 2 * m <= k + 1; m += blockDim.x) {   // f_{k+1}[m] = f_k[m] + gamma conj(f_k[k+1-m])
+      const int mk = k + 1 - m;
+      const double2 fm = f[m], fk = f[mk];
+      const double2 um = cmul(gamma, cconj(fk));
+      if (m == mk) {
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+      } else {
+        const double2 uk = cmul(gamma, cconj(fm));
+        f[m] = make_double2(fm.x + um.x, fm.y + um.y);
+        f[mk] = make_double2(fk.x + uk.x, fk.y + uk.y);
+      }
+    }
+    eps *= 1.0 - (gamma.x * gamma.x + gamma.y * gamma.y);
+    bad = !(eps > 0.0) || !isfinite(eps);
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(flag, 1);
+  const double inv = bad ? nan("") : 1.0 / eps;
+  for (int m = tid; m < b; m += blockDim.x) {
+    const double2 v = f[m];
+    wss[m] = make_double2(v.x * inv, v.y * inv);       // in place when f lives in x's slot
+  }
+}
+
 // K1b: grid (sets, ceil(b / 128)); thread d walks the diagonal j - i = d of B = A^-1.
 __global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restrict__ d_sigma2, int b,
                                                          const double2 *__restrict__ ws, int in_smem,
@@ -279,18 +351,32 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   // f and c in shared memory up to b = 6400, else in the set's workspace (ws: [n_sets][3b + 1] double2)
   const int lev_in_smem = size_t(2) * b * sizeof(double2) <= 200 * 1024;
   const size_t lev_smem = lev_in_smem ? size_t(2) * b * sizeof(double2) : 0;
-  // one warp per set up to b = 256 (no barriers), a 512-thread CTA per set above (the length-k dot product of every
-  // step dominates: config 6, b = 1200, 1.74 ms with one warp)
+  // b <= 256: Levinson-Durbin in one warp (config 4, b = 150: 62 us; the Schur form in one warp: 125 us);
+  // b > 256: the Schur form in a 512-thread CTA (config 6, b = 1200: 0.87 ms; 128 / 256 threads: 1.32 / 0.98 ms;
+  // the CTA Levinson form: 1.34 ms, one warp: 1.74 ms).  CE_K1_SCHUR (experiments): 0 never, 1 always.
+  static const int env_schur = getenv("CE_K1_SCHUR") ? atoi(getenv("CE_K1_SCHUR")) : -1;
   const bool lev_cta = b > 256;
-  if (lev_smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
-    if (e != cudaSuccess) return e;
+  if (env_schur == 1 || (env_schur != 0 && lev_cta)) {
+    const int schur_in_smem = size_t(3) * b * sizeof(double2) <= 200 * 1024;
+    const size_t sch_smem = schur_in_smem ? size_t(3) * b * sizeof(double2) : 0;
+    if (sch_smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(k1_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sch_smem));
+      if (e != cudaSuccess) return e;
+    }
+    static const int env_st = getenv("CE_K1_SCHUR_T") ? atoi(getenv("CE_K1_SCHUR_T")) : K1L_THREADS;   // experiments
+    k1_schur<<<n_sets, std::min(std::max(env_st, 32), K1L_THREADS) / 32 * 32, sch_smem, stream>>>(d_r, d_sigma2, b,
+                                                                                                 d_ws, schur_in_smem, d_flag);
+  } else {
+    if (lev_smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
+      if (e != cudaSuccess) return e;
+    }
+    if (lev_cta)
+      k1_levinson_cta<<<n_sets, K1L_THREADS, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
+    else
+      k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
   }
-  if (lev_cta)
-    k1_levinson_cta<<<n_sets, K1L_THREADS, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
-  else
-    k1_levinson<<<n_sets, 32, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   // one refinement step of x when its five work vectors fit in shared memory (b <= 2560)
