@@ -70,7 +70,7 @@ struct ce_handle {
   ce::Window *d_geo = nullptr;  // [n_win]
   std::vector<ce::Window> geo_tc;   // tensor-core window table (wide windows split into sub-windows)
   ce::Window *d_geo_tc = nullptr;   // [geo_tc.size()]
-  double2 *d_ws = nullptr;      // [n_sets][3b + 1] K1 workspace: x = A^-1 e_0, Levinson vectors (FP64)
+  double2 *d_ws = nullptr;      // [n_sets][4b + 1] K1 workspace: x = A^-1 e_0, recursion / refinement vectors (FP64)
   float2 *d_W = nullptr;        // [n_sets][b][b]
   float2 *d_Wt = nullptr;       // [n_sets][b][b] transposed
   float *d_bank = nullptr;      // K3 filter bank: hi plane then lo plane, [n_sets][nkc][NR][32] each
@@ -264,7 +264,7 @@ int ce_init(const ce_params *p, ce_handle **out) {
   chk(cudaMalloc(&h->d_sigma2, size_t(S) * sizeof(double)));
   chk(cudaMalloc(&h->d_geo, geo.size() * sizeof(ce::Window)));
   chk(cudaMalloc(&h->d_geo_tc, h->geo_tc.size() * sizeof(ce::Window)));
-  chk(cudaMalloc(&h->d_ws, size_t(S) * (3 * size_t(b) + 1) * sizeof(double2)));   // K1 Levinson workspace
+  chk(cudaMalloc(&h->d_ws, size_t(S) * (4 * size_t(b) + 1) * sizeof(double2)));   // K1 Levinson workspace
   chk(cudaMalloc(&h->d_W, size_t(S) * b * b * sizeof(float2)));
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank, 2 * h->bank_plane * sizeof(float)));

@@ -16,8 +16,8 @@
 //       B = (1/x_0) (L1 L1^H - L2 L2^H),  L1 lower-triangular Toeplitz with first column x, L2 with first column
 //       (0, conj(x_{b-1}), ..., conj(x_1)), so along every diagonal
 //       B[i+1][j+1] = B[i][j] + (x[i+1] conj(x[j+1]) - conj(x[b-1-i]) x[b-1-j]) / x_0,   B[0][j] = conj(x[j]);
-//       thread d walks the diagonal j - i = d and writes W = I - sigma^2 B (Hermitian) to both triangles of W and
-//       of W^T (K2's coalesced layout), rounded to complex64.
+//       thread d walks the diagonal j - i = d and writes W = I - sigma^2 B (Hermitian) to the upper triangles of W
+//       and of W^T = conj(W) (K2's coalesced layout), rounded to complex64; K1m mirrors them to the lower triangles.
 //   K1r between them: one step of iterative refinement of x (Levinson-Durbin is only weakly stable).
 // FP64 throughout: an FP32 build alone exceeds the 1e-4 budget at the config-4 condition numbers.
 #include <cuda_runtime.h>
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(32) k1_levinson(const double2 *__restrict__ d_
                                                   int b, double2 *__restrict__ ws, int in_smem, int32_t *__restrict__ flag) {
   extern __shared__ double2 sm1[];
   const int s = blockIdx.x, lane = threadIdx.x;
-  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][c: b][f: b]
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);   // [x: b + 1][c: b][f: b][-: b]
   double2 *c = in_smem ? sm1 : wss + b + 1;          // [b]
   double2 *f = c + b;                                // [b]
   const double2 *r = d_r + size_t(s) * b;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(K1R_THREADS) k1_refine(const double2 *__restri
   extern __shared__ double2 sr[];
   double2 *c = sr, *x = sr + b, *res = sr + 2 * b, *u = sr + 3 * b, *u2 = sr + 4 * b;
   const int s = blockIdx.x, tid = threadIdx.x;
-  double2 *xg = ws + size_t(s) * (3 * size_t(b) + 1);
+  double2 *xg = ws + size_t(s) * (4 * size_t(b) + 1);
   const double2 *r = d_r + size_t(s) * b;
   for (int m = tid; m < b; m += blockDim.x) {
     double2 v = r[m];
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(K1L_THREADS) k1_levinson_cta(const double2 *__
   __shared__ double2 part[2][K1L_THREADS / 32];
   const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = blockDim.x >> 5;
-  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][c: b][f: b]
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);   // [x: b + 1][c: b][f: b][-: b]
   double2 *c = in_smem ? sm1 : wss + b + 1;
   double2 *f = c + b;
   const double2 *r = d_r + size_t(s) * b;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(K1L_THREADS) k1_schur(const double2 *__restric
   extern __shared__ double2 sm1[];
   __shared__ double2 piv[2][2];                      // [step parity][e_k[k+1], R_k[0]]
   const int s = blockIdx.x, tid = threadIdx.x;
-  double2 *wss = ws + size_t(s) * (3 * size_t(b) + 1);   // [x: b + 1][e: b][R: b] (f in x's slot when not in smem)
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);   // [x: b + 1][e: b][R: b] (f in x's slot when not in smem)
   double2 *e = in_smem ? sm1 : wss + b + 1;
   double2 *R = e + b;
   double2 *f = in_smem ? sm1 + 2 * b : wss;
@@ -302,13 +302,129 @@ __global__ void __launch_bounds__(K1L_THREADS) k1_schur(const double2 *__restric
   }
 }
 
+// K1r split over CTAs for large b (grid (sets, ceil(b / 256)), three launches): the refinement's three phases each
+// need the whole previous vector, so each phase is one kernel; every CTA stages the vectors it reads in shared
+// memory and computes 256 outputs.  ws per set: [x: b + 1][res: b][u: b][u2: b].
+constexpr int K1P_THREADS = 256;
+__device__ __forceinline__ double2 first_col(const double2 *r, double sigma2, int m) {
+  const double2 v = r[m];
+  return m == 0 ? make_double2(v.x + sigma2, 0.0) : v;
+}
+__global__ void __launch_bounds__(K1P_THREADS) k1_refine_res(const double2 *__restrict__ d_r,
+                                                             const double *__restrict__ d_sigma2, int b,
+                                                             double2 *__restrict__ ws) {
+  extern __shared__ double2 sp[];
+  double2 *c = sp, *x = sp + b;
+  const int s = blockIdx.x;
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
+  const double2 *r = d_r + size_t(s) * b;
+  const double sigma2 = d_sigma2[s];
+  for (int m = threadIdx.x; m < b; m += blockDim.x) {
+    c[m] = first_col(r, sigma2, m);
+    x[m] = wss[m];
+  }
+  __syncthreads();
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  double2 acc = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+  for (int j = 0; j <= i; ++j) {
+    const double2 p = cmul(c[i - j], x[j]);
+    acc.x -= p.x;
+    acc.y -= p.y;
+  }
+  for (int j = i + 1; j < b; ++j) {
+    const double2 p = cmul(cconj(c[j - i]), x[j]);
+    acc.x -= p.x;
+    acc.y -= p.y;
+  }
+  wss[b + 1 + i] = acc;                              // res
+}
+__global__ void __launch_bounds__(K1P_THREADS) k1_refine_u(int b, double2 *__restrict__ ws) {
+  extern __shared__ double2 sp[];
+  double2 *x = sp, *res = sp + b;
+  const int s = blockIdx.x;
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
+  for (int m = threadIdx.x; m < b; m += blockDim.x) {
+    x[m] = wss[m];
+    res[m] = wss[b + 1 + m];
+  }
+  __syncthreads();
+  const int k = blockIdx.y * blockDim.x + threadIdx.x;
+  if (k >= b) return;
+  double2 a = make_double2(0.0, 0.0), a2 = make_double2(0.0, 0.0);
+  for (int i = k; i < b; ++i) {                      // u[k] = sum_{i>=k} conj(x[i-k]) res[i]
+    const double2 p = cmul(cconj(x[i - k]), res[i]);
+    a.x += p.x;
+    a.y += p.y;
+  }
+  for (int i = k + 1; i < b; ++i) {                  // u2[k] = sum_{i>k} x[b-(i-k)] res[i]
+    const double2 q = cmul(x[b - (i - k)], res[i]);
+    a2.x += q.x;
+    a2.y += q.y;
+  }
+  wss[2 * b + 1 + k] = a;
+  wss[3 * b + 1 + k] = a2;
+}
+__global__ void __launch_bounds__(K1P_THREADS) k1_refine_x(int b, double2 *__restrict__ ws) {
+  extern __shared__ double2 sp[];
+  double2 *x = sp, *u = sp + b, *u2 = sp + 2 * b;
+  const int s = blockIdx.x;
+  double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
+  for (int m = threadIdx.x; m < b; m += blockDim.x) {
+    x[m] = wss[m];
+    u[m] = wss[2 * b + 1 + m];
+    u2[m] = wss[3 * b + 1 + m];
+  }
+  __syncthreads();
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  double2 a = make_double2(0.0, 0.0);
+  for (int k = 0; k <= i; ++k) {                     // delta[i] = (sum_{k<=i} x[i-k] u[k] - sum_{k<i} conj(x[b-i+k]) u2[k]) / x_0
+    const double2 p = cmul(x[i - k], u[k]);
+    a.x += p.x;
+    a.y += p.y;
+  }
+  for (int k = 0; k < i; ++k) {
+    const double2 q = cmul(cconj(x[b - i + k]), u2[k]);
+    a.x -= q.x;
+    a.y -= q.y;
+  }
+  const double ix0 = 1.0 / x[0].x;
+  // the refined x goes to the (now free) res slot: other CTAs of this launch may still be reading x
+  wss[b + 1 + i] = make_double2(x[i].x + a.x * ix0, x[i].y + a.y * ix0);
+}
+
+// K1m: lower triangles of W and W^T from the upper ones through 32 x 32 shared-memory tiles (coalesced reads and
+// writes): W[r][c] = conj(W[c][r]), W^T[r][c] = W[c][r] for r > c.  grid (sets, nb, nb), block (32, 8).
+__global__ void __launch_bounds__(256) k1_mirror(int b, float2 *__restrict__ W, float2 *__restrict__ Wt) {
+  __shared__ float2 tile[32][33];
+  const int s = blockIdx.x, bi = blockIdx.y, bj = blockIdx.z;   // output block row bi, column bj (bi >= bj)
+  if (bi < bj) return;
+  float2 *Ws = W + size_t(s) * b * b;
+  float2 *Wts = Wt + size_t(s) * b * b;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int yy = ty; yy < 32; yy += 8) {              // source: upper block (bj, bi), rows bj*32 + yy
+    const int r = bj * 32 + yy, c = bi * 32 + tx;
+    if (r < b && c < b) tile[yy][tx] = Ws[size_t(r) * b + c];
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {              // destination: lower block (bi, bj), rows bi*32 + yy
+    const int r = bi * 32 + yy, c = bj * 32 + tx;
+    if (r < b && c < b && r > c) {
+      const float2 u = tile[tx][yy];                 // W[c][r]
+      Ws[size_t(r) * b + c] = make_float2(u.x, -u.y);
+      Wts[size_t(r) * b + c] = u;
+    }
+  }
+}
+
 // K1b: grid (sets, ceil(b / 128)); thread d walks the diagonal j - i = d of B = A^-1.
 __global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restrict__ d_sigma2, int b,
-                                                         const double2 *__restrict__ ws, int in_smem,
+                                                         const double2 *__restrict__ ws, int in_smem, int xoff,
                                                          float2 *__restrict__ W, float2 *__restrict__ Wt) {
   extern __shared__ double2 sx[];                    // [b] x, when it fits
   const int s = blockIdx.x;
-  const double2 *xg = ws + size_t(s) * (3 * size_t(b) + 1);
+  const double2 *xg = ws + size_t(s) * (4 * size_t(b) + 1) + xoff;
   if (in_smem)
     for (int m = threadIdx.x; m < b; m += blockDim.x) sx[m] = xg[m];
   __syncthreads();
@@ -326,12 +442,10 @@ __global__ void __launch_bounds__(K1B_THREADS) k1_trench(const double *__restric
     const double2 w = make_double2((i == j ? 1.0 : 0.0) - sigma2 * v.x, -sigma2 * v.y);
     const float2 wu = make_float2(__double2float_rn(w.x), __double2float_rn(w.y));
     const float2 wl = make_float2(wu.x, -wu.y);
+    // upper triangle only (coalesced across the threads of a step); W is Hermitian, so W^T = conj(W) and the
+    // lower triangles are filled by K1m from these
     Ws[size_t(i) * b + j] = wu;                      // W[i][j]
-    Wts[size_t(j) * b + i] = wu;                     // W^T[j][i] = W[i][j]
-    if (d != 0) {
-      Ws[size_t(j) * b + i] = wl;                    // W[j][i] = conj(W[i][j])
-      Wts[size_t(i) * b + j] = wl;                   // W^T[i][j] = W[j][i]
-    }
+    Wts[size_t(i) * b + j] = wl;                     // W^T[i][j] = W[j][i] = conj(W[i][j])
     if (j + 1 < b) {                                 // B[i+1][j+1] = B[i][j] + (x[i+1] x*[j+1] - x*[b-1-i] x[b-1-j]) / x0
       const double2 p = cmul(xs[i + 1], cconj(xs[j + 1]));
       const double2 q = cmul(cconj(xs[b - 1 - i]), xs[b - 1 - j]);
@@ -348,7 +462,7 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
                                 int64_t *launches) {
   (void)N;
   cudaError_t e;
-  // f and c in shared memory up to b = 6400, else in the set's workspace (ws: [n_sets][3b + 1] double2)
+  // f and c in shared memory up to b = 6400, else in the set's workspace (ws: [n_sets][4b + 1] double2)
   const int lev_in_smem = size_t(2) * b * sizeof(double2) <= 200 * 1024;
   const size_t lev_smem = lev_in_smem ? size_t(2) * b * sizeof(double2) : 0;
   // b <= 256: Levinson-Durbin in one warp (config 4, b = 150: 62 us; the Schur form in one warp: 125 us);
@@ -379,9 +493,25 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
-  // one refinement step of x when its five work vectors fit in shared memory (b <= 2560)
+  // one refinement step of x: split over CTAs (three launches) above b = 256, one CTA per set below
+  int xoff = 0;
   const size_t ref_smem = size_t(5) * b * sizeof(double2);
-  if (ref_smem <= 200 * 1024) {
+  const size_t rp_smem = size_t(3) * b * sizeof(double2);
+  if (b > 256 && rp_smem <= 200 * 1024) {
+    if (rp_smem > 48 * 1024) {
+      for (const void *fn : {(const void *)k1_refine_res, (const void *)k1_refine_u, (const void *)k1_refine_x}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rp_smem));
+        if (e != cudaSuccess) return e;
+      }
+    }
+    const dim3 pg(n_sets, (b + K1P_THREADS - 1) / K1P_THREADS);
+    k1_refine_res<<<pg, K1P_THREADS, 2 * size_t(b) * sizeof(double2), stream>>>(d_r, d_sigma2, b, d_ws);
+    k1_refine_u<<<pg, K1P_THREADS, 2 * size_t(b) * sizeof(double2), stream>>>(b, d_ws);
+    k1_refine_x<<<pg, K1P_THREADS, rp_smem, stream>>>(b, d_ws);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches += 3;
+    xoff = b + 1;
+  } else if (ref_smem <= 200 * 1024) {
     if (ref_smem > 48 * 1024) {
       e = cudaFuncSetAttribute(k1_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ref_smem));
       if (e != cudaSuccess) return e;
@@ -397,7 +527,11 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
     if (e != cudaSuccess) return e;
   }
   dim3 grid(n_sets, (b + K1B_THREADS - 1) / K1B_THREADS);
-  k1_trench<<<grid, K1B_THREADS, tr_smem, stream>>>(d_sigma2, b, d_ws, tr_in_smem, d_W, d_Wt);
+  k1_trench<<<grid, K1B_THREADS, tr_smem, stream>>>(d_sigma2, b, d_ws, tr_in_smem, xoff, d_W, d_Wt);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ++*launches;
+  const int nbk = (b + 31) / 32;
+  k1_mirror<<<dim3(n_sets, nbk, nbk), dim3(32, 8), 0, stream>>>(b, d_W, d_Wt);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ++*launches;
   return cudaSuccess;
