@@ -537,7 +537,8 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     if (zsm > 200 * 1024) return fail(CE_EINVAL, "ce_stats_estimate: N too large for the noise kernel");
     // antennas per CTA: enough CTAs for several waves, whole warps of 4-column groups
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     int mpb = env_mpb > 0 ? env_mpb
                           : int(std::min<long long>(M, std::max<long long>(32, (cols / (long long)(nsm * 12)) & ~31LL)));
     mpb = std::max(1, std::min(mpb, M));

@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <vector>
 
@@ -322,15 +323,17 @@ bool gram_launchable(const float2 *y, int32_t K, int32_t N, int32_t D) {
 cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, int32_t K, int32_t N,
                         const int32_t *soi, int32_t n_sets, int32_t D, double *acc, cudaStream_t stream) {
   if (!gram_launchable(y, K, N, D)) return cudaErrorNotSupported;
-  static bool attr = false;
   int dev = 0, nsm = 148;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (!attr) {
+  // the shared-memory opt-in is per device (a process may drive several GPUs)
+  static std::atomic<uint64_t> attr_set{0};
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (!bit || !(attr_set.load() & bit)) {
     e = cudaFuncSetAttribute(k8_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(bit);
   }
   K8Params p;
   p.soi = soi;
