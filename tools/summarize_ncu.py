@@ -17,7 +17,7 @@ G = os.path.join(ROOT, "gpurun_out")
 
 
 def short(name):
-    for k in ("k4_bf16x3", "k5_pair", "k3_tf32x3", "k2_simt", "k1_levinson", "k1_refine", "k1_trench", "k3_build_bank",
+    for k in ("k4_bf16x3", "k5_pair", "k3_tf32x3", "k2_simt", "k1_levinson", "k1_schur", "k1_refine", "k1_trench", "k1_mirror", "k3_build_bank",
               "k4_build_bank"):
         if k in name:
             return k
