@@ -501,7 +501,8 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double *acc = static_cast<double *>(d_work);
   cudaError_t e = cudaMemsetAsync(acc, 0, size_t(n_sets) * (2 * D + 2) * sizeof(double), st);
-  if (e == cudaSuccess && smem > 48 * 1024)
+  // K7a also holds 16 KB of static shared memory: opt in whenever static + dynamic could pass the 48 KB default
+  if (e == cudaSuccess && smem + sizeof(double) * 2 * ce::LB * ce::K7_THREADS > 48 * 1024)
     e = cudaFuncSetAttribute(ce::k7_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) {
     ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));

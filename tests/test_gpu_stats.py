@@ -78,6 +78,18 @@ def test_stats_parity_ragged_shape():
     assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0])
 
 
+def test_stats_parity_wide_band():
+    """N = 2400 tones on the FP32 path (K7a: 16 KB static + 39 KB dynamic shared memory, past the 48 KB default
+    without an opt-in)."""
+    cfg = dataclasses.replace(CONFIGS[2], M=4, K=2, N=2400, b=50, stride=25)
+    x = workload.gen_pilots(cfg, 2)
+    y = workload.gen_instances(cfg, 2, x=x)[:1]
+    r_g, s2_g = _gpu_stats(y, x[:1], 50, 32)
+    r_o, s2_o = oracle.estimate_stats(y, x[:1], 50, 32)
+    assert abs(s2_g[0] / s2_o - 1) < 1e-4
+    assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0])
+
+
 def test_stats_skipped_and_empty_sets():
     cfg = CONFIGS[2]
     x = workload.gen_pilots(cfg, 0)
