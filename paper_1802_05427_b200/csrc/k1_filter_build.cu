@@ -473,7 +473,7 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   if (env_schur == 1 || (env_schur != 0 && lev_cta)) {
     const int schur_in_smem = size_t(3) * b * sizeof(double2) <= 200 * 1024;
     const size_t sch_smem = schur_in_smem ? size_t(3) * b * sizeof(double2) : 0;
-    if (sch_smem > 48 * 1024) {
+    if (sch_smem > 47 * 1024) {   // 1 KB margin: the kernels' pivots / partials are static shared memory
       e = cudaFuncSetAttribute(k1_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sch_smem));
       if (e != cudaSuccess) return e;
     }
@@ -481,7 +481,7 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
     k1_schur<<<n_sets, std::min(std::max(env_st, 32), K1L_THREADS) / 32 * 32, sch_smem, stream>>>(d_r, d_sigma2, b,
                                                                                                  d_ws, schur_in_smem, d_flag);
   } else {
-    if (lev_smem > 48 * 1024) {
+    if (lev_smem > 47 * 1024) {
       e = cudaFuncSetAttribute(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
       if (e != cudaSuccess) return e;

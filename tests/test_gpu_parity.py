@@ -175,13 +175,14 @@ def test_filters_match_oracle():
         est.close()
 
 
-@pytest.mark.parametrize("b,sigma2", [(100, 1e-4), (300, 1e-6), (1200, 1e-3)])
+@pytest.mark.parametrize("b,sigma2", [(100, 1e-4), (300, 1e-6), (1200, 1e-3), (1024, 1e-3), (1536, 1e-3)])
 def test_filters_ill_conditioned_and_full_band(b, sigma2):
     """K1's O(b^2) Toeplitz build (Levinson-Durbin + Trench) on badly conditioned designs: a sparse 8-tap delay
     profile (rank-deficient R_b) with SNR_fixed = 40-60 dB (condition numbers ~1e5-1e8, PAPER.md:306's fixed
-    design regime) and the full-band b = N = 1200 case; same complex64-rounding bar as the matched builds."""
+    design regime), the full-band b = N = 1200 case, and b = 1024 / 1536 where the Schur / Levinson working sets sit
+    just under the 48 KB dynamic shared-memory default; same complex64-rounding bar as the matched builds."""
     ce = _ce()
-    N = 1200
+    N = max(1200, b)
     taps = np.array([0.0, 3.0, 7.5, 12.0, 20.0, 33.0, 41.5, 57.0])      # delays in samples of Nfft = 2048
     p = np.exp(-np.arange(8) / 3.0)
     p /= p.sum()
