@@ -4,7 +4,8 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
 module.  It shares no code with the CUDA path (``paper_1802_05427_b200``):
 window geometry, Toeplitz expansion, LS and the filter are all re-derived here,
-with LU ``solve`` where the GPU uses Cholesky.
+with an LU ``solve`` of the window system (the GPU inverts the Toeplitz matrix by
+Levinson-Durbin + Gohberg-Semencul/Trench; the paper's own solver is ``cposv``).
 
 Everything is plain NumPy/LAPACK in complex128.  Each function cites the
 passage of PAPER.md it follows (line numbers in /root/reference/PAPER.md) and,

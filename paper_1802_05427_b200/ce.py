@@ -203,30 +203,51 @@ class ChannelEstimator:
             raise TypeError("y and x must be complex64")
         if not (y.is_cuda and x.is_cuda):
             raise TypeError("ChannelEstimator.estimate takes CUDA tensors; use estimate_host for host arrays")
+        if y.dim() != 4:
+            raise ValueError(f"y must be [T][M][K][N], got shape {tuple(y.shape)}")
         T, M, K, N = y.shape
         if N != self.N or tuple(x.shape) != (T, K, N):
             raise ValueError(f"shape mismatch: y {tuple(y.shape)}, x {tuple(x.shape)}, N={self.N}")
         if not (y.is_contiguous() and x.is_contiguous()):
             raise ValueError("y and x must be contiguous")
+        if x.device != y.device:
+            raise ValueError("y and x must be on the same device")
         if out is None:
             out = torch.empty_like(y)
+        elif (out.dtype != torch.complex64 or not out.is_cuda or out.device != y.device or
+              tuple(out.shape) != tuple(y.shape) or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous complex64 CUDA tensor with y's shape, on y's device")
         soi = 0
         if set_of_instance is not None:
             if set_of_instance.dtype != torch.int32 or not set_of_instance.is_cuda:
                 raise TypeError("set_of_instance must be a CUDA int32 tensor")
+            if set_of_instance.device != y.device or not set_of_instance.is_contiguous():
+                raise ValueError("set_of_instance must be contiguous and on y's device")
+            if set_of_instance.numel() < T:
+                raise ValueError(f"set_of_instance needs >= T = {T} entries, got {set_of_instance.numel()}")
             soi = set_of_instance.data_ptr()
         ce_estimate(self.handle, y.data_ptr(), x.data_ptr(), out.data_ptr(), T, M, K, soi, _stream_ptr(stream))
         return out
 
-    def estimate_host(self, y: np.ndarray, x: np.ndarray, out: np.ndarray = None, set_of_instance=None,
-                      stream=None):
-        """End-to-end path through ce_estimate_host: host (NumPy or pinned torch) buffers in and out."""
-        T, M, K, N = y.shape
+    def estimate_host(self, y, x, out=None, set_of_instance=None, stream=None):
+        """End-to-end path through ce_estimate_host: host (NumPy or pinned torch) buffers in and out.
+
+        ce_estimate_host copies T*M*K*N elements to and from the raw host pointers, so every shape is checked
+        here before the call (a mismatch would over-read y / x or over-write out)."""
+        if len(tuple(y.shape)) != 4:
+            raise ValueError(f"y must be [T][M][K][N], got shape {tuple(y.shape)}")
+        T, M, K, N = (int(v) for v in y.shape)
+        if N != self.N or tuple(int(v) for v in x.shape) != (T, K, N):
+            raise ValueError(f"shape mismatch: y {tuple(y.shape)}, x {tuple(x.shape)}, N={self.N}")
         if out is None:
-            out = np.empty(y.shape, np.complex64)
+            out = np.empty((T, M, K, N), np.complex64)
+        elif tuple(int(v) for v in out.shape) != (T, M, K, N):
+            raise ValueError(f"out must have y's shape {(T, M, K, N)}, got {tuple(out.shape)}")
         soi_ptr = 0
         if set_of_instance is not None:
-            set_of_instance = np.ascontiguousarray(set_of_instance, np.int32)
+            set_of_instance = np.ascontiguousarray(set_of_instance, np.int32).reshape(-1)
+            if set_of_instance.shape[0] < T:
+                raise ValueError(f"set_of_instance needs >= T = {T} entries, got {set_of_instance.shape[0]}")
             soi_ptr = set_of_instance.ctypes.data
         ce_estimate_host(self.handle, _host_ptr(y), _host_ptr(x), _host_ptr(out), T, M, K, soi_ptr,
                          _stream_ptr(stream))
@@ -354,13 +375,14 @@ def ce_stats_estimate(y, x, D: int, B: int, set_of_instance=None, n_sets: int = 
 
 
 def _host_ptr(a) -> int:
+    """Pointer of a C-contiguous complex64 host array (NumPy, or a CPU / pinned torch tensor)."""
     if isinstance(a, np.ndarray):
         if not a.flags["C_CONTIGUOUS"] or a.dtype != np.complex64:
             raise ValueError("host arrays must be C-contiguous complex64")
         return a.ctypes.data
-    # torch CPU tensor (possibly pinned)
-    if a.is_cuda or not a.is_contiguous():
-        raise ValueError("host tensors must be contiguous CPU tensors")
+    import torch
+    if not isinstance(a, torch.Tensor) or a.is_cuda or not a.is_contiguous() or a.dtype != torch.complex64:
+        raise ValueError("host tensors must be contiguous complex64 CPU tensors")
     return a.data_ptr()
 
 

@@ -95,18 +95,7 @@ struct ce_handle {
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  bool ok = true;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
-    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
+using ce::DeviceGuard;
 
 int fail(int status, const std::string &msg) {
   set_last_error(msg);
@@ -157,9 +146,11 @@ bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
 int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
   if (T < 1 || M < 1 || K < 1)
     return fail(CE_EINVAL, "T, M and K must be >= 1");
-  // 64-bit element count; the kernels index with 64-bit offsets.
+  // 64-bit element count; the kernels index elements with 64-bit offsets, but columns (T*M*K rows of N tones)
+  // with 32-bit integers
   const long double elems = (long double)T * M * K * h->N;
   if (elems > 4.0e12L) return fail(CE_EINVAL, "problem too large");
+  if ((long long)T * M * K >= (1LL << 31)) return fail(CE_EINVAL, "T*M*K must be < 2^31 (column index range)");
   return CE_OK;
 }
 
@@ -167,7 +158,10 @@ int check_sizes(const ce_handle *h, int32_t T, int32_t M, int32_t K) {
 
 extern "C" {
 
-const char *ce_version(void) { return "libce 0.3 sm_100a (K1 fp64 cholesky, K2 fp32 simt, K3 tcgen05 tf32x3, K4 tcgen05 bf16x3 + TMA, K5 cta-pair bf16x3 resident bank)"; }
+const char *ce_version(void) {
+  return "libce 0.4 sm_100a (K1 fp64 Levinson/Schur + refinement + Gohberg-Semencul/Trench, K2 fp32 simt, K3 tcgen05 "
+         "tf32x3, K4 tcgen05 bf16x3 + TMA, K5 tcgen05 cta-pair bf16x3 with the filter resident in TMEM)";
+}
 
 const char *ce_status_string(int status) {
   switch (status) {

@@ -73,4 +73,32 @@ cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, 
 
 void set_last_error(const std::string &msg);
 
+// Selects a handle's device for the duration of an entry point and restores the caller's current device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
+// Dynamic shared-memory opt-in: a launch needs cudaFuncAttributeMaxDynamicSharedMemorySize >= dyn whenever dyn plus
+// the kernel's own static __shared__ storage exceeds the 48 KB default.  The static size is read from the compiled
+// kernel (cudaFuncGetAttributes), so a later change to a kernel's __shared__ arrays cannot silently break the launch.
+inline cudaError_t smem_opt_in(const void *fn, size_t dyn) {
+  if (dyn == 0) return cudaSuccess;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  if (dyn + fa.sharedSizeBytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+}
+
 }  // namespace ce

@@ -310,45 +310,52 @@ __device__ __forceinline__ double2 first_col(const double2 *r, double sigma2, in
   const double2 v = r[m];
   return m == 0 ? make_double2(v.x + sigma2, 0.0) : v;
 }
+// in_smem = 0 (b beyond the shared-memory range): the same arithmetic on the vectors in the set's workspace and
+// the statistics column in global memory (L2-resident at these sizes)
 __global__ void __launch_bounds__(K1P_THREADS) k1_refine_res(const double2 *__restrict__ d_r,
                                                              const double *__restrict__ d_sigma2, int b,
-                                                             double2 *__restrict__ ws) {
+                                                             double2 *__restrict__ ws, int in_smem) {
   extern __shared__ double2 sp[];
-  double2 *c = sp, *x = sp + b;
   const int s = blockIdx.x;
   double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
   const double2 *r = d_r + size_t(s) * b;
   const double sigma2 = d_sigma2[s];
-  for (int m = threadIdx.x; m < b; m += blockDim.x) {
-    c[m] = first_col(r, sigma2, m);
-    x[m] = wss[m];
+  double2 *c = sp;
+  const double2 *x = in_smem ? sp + b : wss;
+  if (in_smem) {
+    for (int m = threadIdx.x; m < b; m += blockDim.x) {
+      c[m] = first_col(r, sigma2, m);
+      sp[b + m] = wss[m];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int i = blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= b) return;
   double2 acc = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
   for (int j = 0; j <= i; ++j) {
-    const double2 p = cmul(c[i - j], x[j]);
+    const double2 p = cmul(in_smem ? c[i - j] : first_col(r, sigma2, i - j), x[j]);
     acc.x -= p.x;
     acc.y -= p.y;
   }
   for (int j = i + 1; j < b; ++j) {
-    const double2 p = cmul(cconj(c[j - i]), x[j]);
+    const double2 p = cmul(cconj(in_smem ? c[j - i] : first_col(r, sigma2, j - i)), x[j]);
     acc.x -= p.x;
     acc.y -= p.y;
   }
   wss[b + 1 + i] = acc;                              // res
 }
-__global__ void __launch_bounds__(K1P_THREADS) k1_refine_u(int b, double2 *__restrict__ ws) {
+__global__ void __launch_bounds__(K1P_THREADS) k1_refine_u(int b, double2 *__restrict__ ws, int in_smem) {
   extern __shared__ double2 sp[];
-  double2 *x = sp, *res = sp + b;
   const int s = blockIdx.x;
   double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
-  for (int m = threadIdx.x; m < b; m += blockDim.x) {
-    x[m] = wss[m];
-    res[m] = wss[b + 1 + m];
+  const double2 *x = in_smem ? sp : wss, *res = in_smem ? sp + b : wss + b + 1;
+  if (in_smem) {
+    for (int m = threadIdx.x; m < b; m += blockDim.x) {
+      sp[m] = wss[m];
+      sp[b + m] = wss[b + 1 + m];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int k = blockIdx.y * blockDim.x + threadIdx.x;
   if (k >= b) return;
   double2 a = make_double2(0.0, 0.0), a2 = make_double2(0.0, 0.0);
@@ -365,17 +372,20 @@ __global__ void __launch_bounds__(K1P_THREADS) k1_refine_u(int b, double2 *__res
   wss[2 * b + 1 + k] = a;
   wss[3 * b + 1 + k] = a2;
 }
-__global__ void __launch_bounds__(K1P_THREADS) k1_refine_x(int b, double2 *__restrict__ ws) {
+__global__ void __launch_bounds__(K1P_THREADS) k1_refine_x(int b, double2 *__restrict__ ws, int in_smem) {
   extern __shared__ double2 sp[];
-  double2 *x = sp, *u = sp + b, *u2 = sp + 2 * b;
   const int s = blockIdx.x;
   double2 *wss = ws + size_t(s) * (4 * size_t(b) + 1);
-  for (int m = threadIdx.x; m < b; m += blockDim.x) {
-    x[m] = wss[m];
-    u[m] = wss[2 * b + 1 + m];
-    u2[m] = wss[3 * b + 1 + m];
+  const double2 *x = in_smem ? sp : wss, *u = in_smem ? sp + b : wss + 2 * b + 1,
+                *u2 = in_smem ? sp + 2 * b : wss + 3 * b + 1;
+  if (in_smem) {
+    for (int m = threadIdx.x; m < b; m += blockDim.x) {
+      sp[m] = wss[m];
+      sp[b + m] = wss[2 * b + 1 + m];
+      sp[2 * b + m] = wss[3 * b + 1 + m];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int i = blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= b) return;
   double2 a = make_double2(0.0, 0.0);
@@ -473,19 +483,13 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   if (env_schur == 1 || (env_schur != 0 && lev_cta)) {
     const int schur_in_smem = size_t(3) * b * sizeof(double2) <= 200 * 1024;
     const size_t sch_smem = schur_in_smem ? size_t(3) * b * sizeof(double2) : 0;
-    if (sch_smem > 47 * 1024) {   // 1 KB margin: the kernels' pivots / partials are static shared memory
-      e = cudaFuncSetAttribute(k1_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sch_smem));
-      if (e != cudaSuccess) return e;
-    }
+    if ((e = smem_opt_in((const void *)k1_schur, sch_smem)) != cudaSuccess) return e;
     static const int env_st = getenv("CE_K1_SCHUR_T") ? atoi(getenv("CE_K1_SCHUR_T")) : K1L_THREADS;   // experiments
     k1_schur<<<n_sets, std::min(std::max(env_st, 32), K1L_THREADS) / 32 * 32, sch_smem, stream>>>(d_r, d_sigma2, b,
                                                                                                  d_ws, schur_in_smem, d_flag);
   } else {
-    if (lev_smem > 47 * 1024) {
-      e = cudaFuncSetAttribute(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(lev_smem));
-      if (e != cudaSuccess) return e;
-    }
+    e = smem_opt_in(lev_cta ? (const void *)k1_levinson_cta : (const void *)k1_levinson, lev_smem);
+    if (e != cudaSuccess) return e;
     if (lev_cta)
       k1_levinson_cta<<<n_sets, K1L_THREADS, lev_smem, stream>>>(d_r, d_sigma2, b, d_ws, lev_in_smem, d_flag);
     else
@@ -497,35 +501,29 @@ cudaError_t launch_filter_build(const double2 *d_r, const double *d_sigma2, int3
   int xoff = 0;
   const size_t ref_smem = size_t(5) * b * sizeof(double2);
   const size_t rp_smem = size_t(3) * b * sizeof(double2);
-  if (b > 256 && rp_smem <= 200 * 1024) {
-    if (rp_smem > 48 * 1024) {
-      for (const void *fn : {(const void *)k1_refine_res, (const void *)k1_refine_u, (const void *)k1_refine_x}) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rp_smem));
-        if (e != cudaSuccess) return e;
-      }
-    }
+  if (b > 256) {
+    // every b: the vectors in shared memory up to b = 4266 (3b double2 <= 200 KB), else read from the workspace
+    const int rp_in = rp_smem <= 200 * 1024;
     const dim3 pg(n_sets, (b + K1P_THREADS - 1) / K1P_THREADS);
-    k1_refine_res<<<pg, K1P_THREADS, 2 * size_t(b) * sizeof(double2), stream>>>(d_r, d_sigma2, b, d_ws);
-    k1_refine_u<<<pg, K1P_THREADS, 2 * size_t(b) * sizeof(double2), stream>>>(b, d_ws);
-    k1_refine_x<<<pg, K1P_THREADS, rp_smem, stream>>>(b, d_ws);
+    const size_t s2b = rp_in ? 2 * size_t(b) * sizeof(double2) : 0, s3b = rp_in ? rp_smem : 0;
+    if ((e = smem_opt_in((const void *)k1_refine_res, s2b)) != cudaSuccess) return e;
+    if ((e = smem_opt_in((const void *)k1_refine_u, s2b)) != cudaSuccess) return e;
+    if ((e = smem_opt_in((const void *)k1_refine_x, s3b)) != cudaSuccess) return e;
+    k1_refine_res<<<pg, K1P_THREADS, s2b, stream>>>(d_r, d_sigma2, b, d_ws, rp_in);
+    k1_refine_u<<<pg, K1P_THREADS, s2b, stream>>>(b, d_ws, rp_in);
+    k1_refine_x<<<pg, K1P_THREADS, s3b, stream>>>(b, d_ws, rp_in);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches += 3;
     xoff = b + 1;
   } else if (ref_smem <= 200 * 1024) {
-    if (ref_smem > 48 * 1024) {
-      e = cudaFuncSetAttribute(k1_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ref_smem));
-      if (e != cudaSuccess) return e;
-    }
+    if ((e = smem_opt_in((const void *)k1_refine, ref_smem)) != cudaSuccess) return e;
     k1_refine<<<n_sets, K1R_THREADS, ref_smem, stream>>>(d_r, d_sigma2, b, d_ws);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++*launches;
   }
   const int tr_in_smem = size_t(b) * sizeof(double2) <= 200 * 1024;
   const size_t tr_smem = tr_in_smem ? size_t(b) * sizeof(double2) : 0;
-  if (tr_smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k1_trench, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tr_smem));
-    if (e != cudaSuccess) return e;
-  }
+  if ((e = smem_opt_in((const void *)k1_trench, tr_smem)) != cudaSuccess) return e;
   dim3 grid(n_sets, (b + K1B_THREADS - 1) / K1B_THREADS);
   k1_trench<<<grid, K1B_THREADS, tr_smem, stream>>>(d_sigma2, b, d_ws, tr_in_smem, xoff, d_W, d_Wt);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

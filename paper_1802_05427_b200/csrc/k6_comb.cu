@@ -342,7 +342,8 @@ int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out) {
 
 int ce_comb_build_filters(ce_comb_handle *h, void *stream) {
   if (h == nullptr) return cfail(CE_EINVAL, "ce_comb_build_filters: NULL handle");
-  cudaSetDevice(h->device);
+  ce::DeviceGuard dg(h->device);
+  if (!dg.ok) return cfail(CE_ECUDA, "ce_comb_build_filters: cannot select the handle's device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->built = false;
   cudaError_t e = cudaMemsetAsync(h->d_flag, 0, sizeof(int32_t), st);
@@ -375,7 +376,8 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
   const size_t nh = rows * h->g.n_ue * h->g.N * 8, ny = rows * h->g.N * 8, nx = size_t(T) * h->g.N * 8;
   if ((hy < yy + ny && yy < hy + nh) || (hy < xx + nx && xx < hy + nh))
     return cfail(CE_EINVAL, "ce_comb_estimate: output aliases an input");
-  cudaSetDevice(h->device);
+  ce::DeviceGuard dg(h->device);
+  if (!dg.ok) return cfail(CE_ECUDA, "ce_comb_estimate: cannot select the handle's device");
   const ce::CombGeo &g = h->g;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float2 *yp = static_cast<const float2 *>(d_y), *xp = static_cast<const float2 *>(d_x);
@@ -390,21 +392,19 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
     if (blocks > 0x7fffffffULL) return cfail(CE_EINVAL, "ce_comb_estimate: too many rows");
     cudaError_t e;
     if (g.mode == CE_COMB_FULL) {
-      e = cudaFuncSetAttribute(ce::k6_estimate_g<0, 12, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_g));
+      e = ce::smem_opt_in((const void *)ce::k6_estimate_g<0, 12, 12>, smem_g);
       if (e == cudaSuccess)
         ce::k6_estimate_g<0, 12, 12><<<unsigned(blocks), 128, smem_g, st>>>(yp, xp, h->d_W, hp, M, g);
     } else {
-      e = cudaFuncSetAttribute(ce::k6_estimate_g<1, 3, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_g));
+      e = ce::smem_opt_in((const void *)ce::k6_estimate_g<1, 3, 12>, smem_g);
       if (e == cudaSuccess)
         ce::k6_estimate_g<1, 3, 12><<<unsigned(blocks), 128, smem_g, st>>>(yp, xp, h->d_W, hp, M, g);
     }
     if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: smem attribute");
   } else {
     const size_t smem = size_t(g.N) * sizeof(float2);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(ce::k6_estimate, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: smem attribute");
-    }
+    cudaError_t e = ce::smem_opt_in((const void *)ce::k6_estimate, smem);
+    if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: smem attribute");
     ce::k6_estimate<<<unsigned(rows), 256, smem, st>>>(yp, xp, h->d_W, hp, M, g);
   }
   cudaError_t e = cudaGetLastError();
@@ -416,7 +416,8 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
 int ce_comb_get_filters(ce_comb_handle *h, void *host_W) {
   if (h == nullptr || host_W == nullptr) return cfail(CE_EINVAL, "ce_comb_get_filters: NULL argument");
   if (!h->built) return cfail(CE_ESTATE, "ce_comb_get_filters: filters not built");
-  cudaSetDevice(h->device);
+  ce::DeviceGuard dg(h->device);
+  if (!dg.ok) return cfail(CE_ECUDA, "ce_comb_get_filters: cannot select the handle's device");
   cudaError_t e = cudaMemcpy(host_W, h->d_W, filt_elems(h->g) * sizeof(float2), cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? CE_OK : ccuda(e, "ce_comb_get_filters");
 }
@@ -429,10 +430,12 @@ int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out) {
 
 int ce_comb_free(ce_comb_handle *h) {
   if (h == nullptr) return CE_OK;
-  cudaSetDevice(h->device);
-  cudaFree(h->d_r);
-  cudaFree(h->d_W);
-  cudaFree(h->d_flag);
+  {
+    ce::DeviceGuard dg(h->device);
+    cudaFree(h->d_r);
+    cudaFree(h->d_W);
+    cudaFree(h->d_flag);
+  }
   delete h;
   return CE_OK;
 }

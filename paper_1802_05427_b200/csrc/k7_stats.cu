@@ -501,9 +501,8 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double *acc = static_cast<double *>(d_work);
   cudaError_t e = cudaMemsetAsync(acc, 0, size_t(n_sets) * (2 * D + 2) * sizeof(double), st);
-  // K7a also holds 16 KB of static shared memory: opt in whenever static + dynamic could pass the 48 KB default
-  if (e == cudaSuccess && smem + sizeof(double) * 2 * ce::LB * ce::K7_THREADS > 48 * 1024)
-    e = cudaFuncSetAttribute(ce::k7_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  // K7a also holds static shared memory: ce::smem_opt_in reads its size from the compiled kernel
+  if (e == cudaSuccess) e = ce::smem_opt_in((const void *)ce::k7_accumulate, smem);
   if (e != cudaSuccess) {
     ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
     return CE_ECUDA;
@@ -545,7 +544,7 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     mpb = std::max(1, std::min(mpb, M));
     const long long zctas = (long long)T * K * ((M + mpb - 1) / mpb);
     if (zctas > 0x7fffffffLL) return fail(CE_EINVAL, "ce_stats_estimate: too many columns");
-    e = cudaFuncSetAttribute(ce::k7_noise, cudaFuncAttributeMaxDynamicSharedMemorySize, int(zsm));
+    e = ce::smem_opt_in((const void *)ce::k7_noise, zsm);
     if (e != cudaSuccess) {
       ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
       return CE_ECUDA;

@@ -9,6 +9,7 @@ import pytest
 
 import oracle
 import workload
+from _parity import assert_parity
 from workload import CONFIGS
 
 torch = pytest.importorskip("torch")
@@ -71,9 +72,7 @@ def test_config_parity_full(cfg_id, kernel):
     r, s2, x, y, soi = _inputs(cfg)
     h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
-    err = oracle.rel_fro_error_per_instance(h, ref)
-    assert np.all(err <= TOL), err
-    assert np.isfinite(h).all()
+    assert_parity(h, ref, cfg.N, cfg.b, cfg.stride)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -84,8 +83,7 @@ def test_config4_parity_antenna_subset(kernel):
     r, s2, x, y, soi = _inputs(cfg, m_hi=16)
     h = _run(cfg.N, cfg.b, cfg.stride, r, s2, y, x, soi, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, soi, cfg.b, cfg.stride)
-    err = oracle.rel_fro_error_per_instance(h, ref)
-    assert np.all(err <= TOL), err
+    assert_parity(h, ref, cfg.N, cfg.b, cfg.stride)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -112,7 +110,7 @@ def test_full_size_sampled(cfg_id, kernel):
             y_tm = y_d[t, m:m + 1].cpu().numpy()[None]
             ref = oracle.block_lmmse(y_tm, x[t:t + 1], r, s2, soi[t:t + 1], cfg.b, cfg.stride)
             got = h[t, m:m + 1].cpu().numpy()[None]
-            assert oracle.rel_fro_error_per_instance(got, ref)[0] <= TOL, (t, m)
+            assert_parity(got, ref, cfg.N, cfg.b, cfg.stride)
     # properties at full size: finite everywhere, output energy ~ channel energy (sum p = 1)
     assert torch.isfinite(torch.view_as_real(h)).all()
     p = (h.abs() ** 2).mean().item()
@@ -127,7 +125,7 @@ def test_full_size_sampled(cfg_id, kernel):
     (96, 96, 96, 2, 3, 1),     # b = N: full LMMSE
     (40, 1, 1, 4, 2, 1),       # b = 1: scalar Wiener
     (40, 8, 1, 5, 3, 2),       # stride 1: maximal overlap
-    (300, 256, 44, 2, 2, 1),   # large b: K1 Cholesky in global memory, > 3 K2 row tiles
+    (300, 256, 44, 2, 2, 1),   # large b: K1 Levinson + Trench, > 3 K2 row tiles
     (130, 65, 64, 11, 7, 3),   # cols = 77 spans two column tiles with a ragged tail
 ])
 def test_edge_shapes(N, b, s, M, K, T, kernel):
@@ -143,7 +141,7 @@ def test_edge_shapes(N, b, s, M, K, T, kernel):
     x = np.exp(2j * np.pi * rng.random((T, K, N))).astype(np.complex64) * np.float32(1.7)  # non-unit pilots
     h = _run(N, b, s, r, s2, y, x, kernel=kernel)
     ref = oracle.block_lmmse(y, x, r, s2, None, b, s)
-    assert np.all(oracle.rel_fro_error_per_instance(h, ref) <= TOL)
+    assert_parity(h, ref, N, b, s)
     if b == N:
         full = oracle.full_lmmse(y, x, r, s2, None)
         assert np.all(oracle.rel_fro_error_per_instance(h, full) <= TOL)
