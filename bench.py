@@ -37,11 +37,20 @@ L2_BYTES = 126 * 1024 * 1024
 
 
 def _peaks():
+    """MEASURED_PEAKS.json (driver-written: HBM copy, cuBLAS bf16) plus the committed FFMA microbenchmark
+    (profiles/ffma_peak_r02.json, tools/ffma_peak.cu run on this pool's B200s) as fp32_tflops."""
+    d = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
+            d = json.load(f)
     except Exception:
-        return {}
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "ffma_peak_r02.json")) as f:
+            d["fp32_tflops"] = float(json.load(f)["fp32_tflops_burst"])
+    except Exception:
+        pass
+    return d
 
 
 class ClockSampler:
@@ -504,6 +513,8 @@ def run_ours(args, cfg):
     res = time_estimator(est, ys, hs, x_d, soi_d, args.steps, args.warmup, args.launch, dist,
                          clock_s=args.clock_window_s)
     ms_max = res["ms_max"]
+    m_par = max(1, min(cfg.M, args.ref_antennas * 4))
+    h_sample = hs[0][:1, :min(m_par, m_hi - m_lo)].cpu().numpy()   # parity sample, before the buffers are reused
     E_glob = cfg.estimates * M_glob // cfg.M          # estimates of the whole job per step
     E = cfg.estimates * (m_hi - m_lo) // cfg.M        # this rank's estimates per launch (roofline)
     value = E_glob * args.steps / (ms_max * 1e-3)
@@ -562,7 +573,7 @@ def run_ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the oracle as it stands, on a bounded sample of the same workload (antennas [0, m) of instance 0),
         # all host cores then one core; its output doubles as the parity sample of the timed buffers
-        m = max(1, min(cfg.M, args.ref_antennas * 4))
+        m = h_sample.shape[1]
         times, ref = _oracle_sample_timing(cfg, x[:1], y[:1, :m], r, s2, soi[:1], budget_s=args.cpu_budget_s)
         times1, _ = _oracle_sample_timing(cfg, x[:1], y[:1, :m], r, s2, soi[:1], budget_s=args.cpu_budget_s / 2,
                                           threads=1)
@@ -576,7 +587,7 @@ def run_ours(args, cfg):
                               "note": "BLAS limited to 1 thread (threadpoolctl): per-core figure beside the paper's "
                                       "Table V per-core cycle counts (PAPER.md:545-548)"}}
         import oracle
-        h0 = hs[0][:1, :m].cpu().numpy().astype(np.complex128)     # every y buffer holds the same draw
+        h0 = h_sample.astype(np.complex128)                          # every y buffer holds the same draw
         d = (h0 - ref).reshape(-1, N)
         row_err = 0.0
         for (_a, o, o1) in oracle.window_table(N, cfg.b, cfg.stride):

@@ -91,6 +91,7 @@ int main(int argc, char **argv) {
   std::sort(rates.begin(), rates.end());
   const double ghz = rates.empty() ? 1.965 : rates[rates.size() / 2];
   printf("effective clock %.3f GHz (median over CTAs; %zu CTAs)\n", ghz, rates.size());
+  printf("grid: CTAs with a trace %s\n", kernel == 4 ? "(K5 pairs)" : "");
   const char *names[256] = {};
   names[2] = "setup done";
   names[3] = "epi warp done";
@@ -111,6 +112,20 @@ int main(int argc, char **argv) {
     std::sort(v.begin(), v.end());
     const char *nm = names[slot];
     char buf[64];
+    if (!nm && kernel == 4) {
+      if (slot >= 8 && slot < 32) snprintf(buf, 64, "raw TMA issue it=%d", slot - 8);
+      else if (slot >= 32 && slot < 56) snprintf(buf, 64, "raw full seen it=%d", slot - 32);
+      else if (slot >= 56 && slot < 80) snprintf(buf, 64, "B written it=%d", slot - 56);
+      else if (slot >= 80 && slot < 104) snprintf(buf, 64, "W piece consumed pp=%d", slot - 80);
+      else if (slot >= 104 && slot < 128) snprintf(buf, 64, "MMA b_full passed it=%d", slot - 104);
+      else if (slot >= 128 && slot < 136) snprintf(buf, 64, "tile MMAs committed lt=%d", slot - 128);
+      else if (slot >= 136 && slot < 144) snprintf(buf, 64, "epi start lt=%d", slot - 136);
+      else if (slot < 152) snprintf(buf, 64, "epi done lt=%d", slot - 144);
+      else if (slot < 160) snprintf(buf, 64, "MMA w_full passed e=%d", slot - 152);
+      else if (slot < 168) snprintf(buf, 64, "W load start e=%d", slot - 160);
+      else snprintf(buf, 64, "W load done e=%d", slot - 168);
+      nm = buf;
+    }
     if (!nm) {
       if (slot >= 8 && slot < 32) snprintf(buf, 64, "raw TMA issue it=%d", slot - 8);
       else if (slot >= 32 && slot < 56) snprintf(buf, 64, "raw full seen it=%d", slot - 32);

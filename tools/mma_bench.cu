@@ -106,6 +106,119 @@ __global__ void __cluster_dims__(2, 1, 1) bench_pair(int iters, int N, unsigned 
   }
 }
 
+__device__ __forceinline__ void mma2_ts_b(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// CTA pair, A from TMEM (K5's form): M = 256, N columns, N/2 B rows per CTA in SW64 smem; commit every `cevery` MMAs
+__global__ void __cluster_dims__(2, 1, 1) bench_pair_ts(int iters, int N, int cevery, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t *smem = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc2(&slot, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t d = slot;
+  if (threadIdx.x == 0 && cluster_ctarank() == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+    const uint64_t bd = sw64_desc(smem_u32(smem + 32 * 1024));
+    unsigned long long t0 = clock64();
+    int ph = 0, n = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int ks = 0; ks < 2; ++ks) {
+        mma2_ts_b(d, d + 256 + 8 * ks, bd + uint64_t(2 * ks), idesc, (it | ks) != 0);
+        if (++n == cevery) {
+          n = 0;
+          mma_commit_pair(&bar);
+        }
+      }
+      if ((it & 15) == 15) {
+        mma_commit_pair(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+        if (cevery < 1000) {   // the per-chunk commits also arrived: drain by waiting the phase parity again
+        }
+      }
+    }
+    mma_commit_pair(&bar);
+    mbar_wait(&bar, ph);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc2(d, 512);
+  }
+}
+
+// single CTA, A from TMEM: M = 128, N columns (D at columns 0.., A at columns 256..)
+__global__ void bench_ts1(int iters, int N, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t *smem = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t d = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    const uint64_t bd = sw64_desc(smem_u32(smem + 32 * 1024));
+    unsigned long long t0 = clock64();
+    int ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t a = d + 256 + 8 * ks;
+        const uint32_t acc = (it | ks) != 0;
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+            "r"(a), "l"(bd + uint64_t(2 * ks)), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+      if ((it & 15) == 15) {
+        mma_commit(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, ph);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(d, 512);
+  }
+}
+
 int main() {
   unsigned long long *dout, h[148];
   cudaMalloc(&dout, 148 * 8);
@@ -136,6 +249,28 @@ int main() {
     const double c = double(h[0]) / (iters * 2);
     printf("PAIR M=256 N=%3d: %.1f cyc/MMA (%.0f flop/clk per SM)  %s\n", N, c, 2.0 * 128 * N * 16 / c,
            cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFuncSetAttribute(bench_ts1, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int N : {256, 208, 128, 64}) {
+    const int iters = 4096;
+    bench_ts1<<<148, 128, 100 * 1024>>>(iters, N, dout);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, dout, 8, cudaMemcpyDeviceToHost);
+    const double c = double(h[0]) / (iters * 2);
+    printf("TS1 (A in TMEM) M=128 N=%3d: %.1f cyc/MMA (%.0f flop/clk)  %s\n", N, c, 2.0 * 128 * N * 16 / c,
+           cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFuncSetAttribute(bench_pair_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int N : {256, 128, 96, 64}) {
+    for (int grid : {2, 148}) {
+      const int iters = 4096;
+      bench_pair_ts<<<grid, 128, 100 * 1024>>>(iters, N, 1 << 30, dout);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, dout, 8, cudaMemcpyDeviceToHost);
+      const double c = double(h[0]) / (iters * 2);
+      printf("PAIR TS (A in TMEM) M=256 N=%3d grid %3d: %.1f cyc/MMA (%.0f flop/clk per SM)  %s\n", N, grid, c,
+             2.0 * 128 * N * 16 / c, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
