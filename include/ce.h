@@ -58,11 +58,12 @@ typedef enum {
 
 typedef enum {
   CE_KERNEL_AUTO = 0,   /* library picks the fastest kernel meeting the 1e-4 parity bar */
-  CE_KERNEL_SIMT = 1,   /* K2: FP32 SIMT complex FMA contraction */
+  CE_KERNEL_SIMT = 1,   /* K2: FP32 SIMT complex FMA contraction (fallback when the tensor-core filter banks do not
+                           fit; north_star's SIMT design, kept for parity and as the FP32 reference path) */
   CE_KERNEL_TF32X3 = 2, /* K3: tcgen05 kind::tf32, error-compensated hi/lo split (3 MMAs) */
-  CE_KERNEL_BF16X3 = 3, /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring */
-  CE_KERNEL_BF16X3_PAIR = 4 /* K5: K4's arithmetic on a CTA pair (cta_group::2, M = 256) with the filter
-                               half-bank resident in shared memory */
+  CE_KERNEL_BF16X3 = 3  /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring */
+  /* 4 was the CTA-pair kernel K5 (filter stationary in TMEM): removed in round 2 -- exact, but pair MMAs with the
+   * A operand in TMEM cost 180 cycles flat and it ran 2.6-4.5x slower than K4; 4 is now CE_EINVAL */
 } ce_kernel;
 
 typedef struct ce_handle ce_handle; /* opaque */
@@ -122,18 +123,16 @@ int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void 
 /* Free W, workspace, staging buffers and the handle.  NULL is allowed (no-op). */
 int ce_free(ce_handle *h);
 
-/* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value, or for a tensor-core
- * kernel when some window does not fit its tile (2*kept + (2*(o_w-a_w) mod 8) > 256).
- * CE_KERNEL_AUTO (default): BF16X3 when it fits and the call is launchable (K <= 32, N even, every window
- * start a_w even, 16-byte aligned y/x), else TF32X3 when it fits, else SIMT.  BF16X3_PAIR is explicit only
- * (it also needs the resident half-bank plus 3 input stages to fit in shared memory; measured slower than
- * BF16X3 on configs 3-5).
- * All meet the 1e-4 parity bar.
- * An explicit BF16X3 / BF16X3_PAIR is rejected here when a window start is odd, and by ce_estimate
- * (CE_EINVAL) when the call itself is not launchable for it. */
+/* Choose the contraction kernel (ce_kernel).  CE_EINVAL for an unknown value (including the retired 4), for a
+ * tensor-core kernel when its filter banks would exceed 8 GB (very large b x n_sets), and for BF16X3 when some
+ * window start a_w is odd (16-byte TMA boxes).  Windows wider than one 256-column accumulator are split into
+ * output sub-windows over the same input, so every b fits the tensor-core tiles.
+ * CE_KERNEL_AUTO (default): BF16X3 when the call is launchable (K <= 32, N even, every window start a_w even,
+ * 16-byte aligned y/x), else TF32X3, else SIMT.  All meet the 1e-4 parity bar.
+ * An explicit BF16X3 is also rejected by ce_estimate (CE_EINVAL) when the call itself is not launchable for it. */
 int ce_set_kernel(ce_handle *h, int32_t kernel);
 
-/* The kernel the most recent ce_estimate launched (CE_KERNEL_SIMT / _TF32X3 / _BF16X3 / _BF16X3_PAIR); before
+/* The kernel the most recent ce_estimate launched (CE_KERNEL_SIMT / _TF32X3 / _BF16X3); before
  * the first estimate, the kernel AUTO/the setting prefers for this geometry. */
 int ce_selected_kernel(const ce_handle *h, int32_t *out);
 

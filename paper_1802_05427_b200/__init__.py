@@ -13,7 +13,6 @@ from .ce import (  # noqa: F401
     CE_ESTATE,
     CE_KERNEL_AUTO,
     CE_KERNEL_BF16X3,
-    CE_KERNEL_BF16X3_PAIR,
     CE_KERNEL_SIMT,
     CE_KERNEL_TF32X3,
     CE_OK,

@@ -23,7 +23,7 @@ if not os.path.exists(_LIB_PATH):
 lib = ctypes.CDLL(_LIB_PATH)
 
 CE_OK, CE_EINVAL, CE_ENOMEM, CE_ECUDA, CE_ENOTPD, CE_ESTATE, CE_ENODEV = 0, -1, -2, -3, -4, -5, -6
-CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3, CE_KERNEL_BF16X3, CE_KERNEL_BF16X3_PAIR = 0, 1, 2, 3, 4
+CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3, CE_KERNEL_BF16X3 = 0, 1, 2, 3   # 4 (K5) retired: CE_EINVAL
 
 # every function declared in include/ce.h (tests check the .so exports all of them)
 EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",

@@ -78,9 +78,6 @@ struct ce_handle {
   bool tf32_ok = false;         // the tensor-core filter banks fit (any b; wide windows are split)
   uint16_t *d_bank16 = nullptr; // K4 filter bank: bf16 hi plane then lo plane
   size_t bank16_plane = 0;      // elements per plane
-  bool pair_ok = false;         // K5's filter TMEM image fits (b <= 208) and every window start is even
-  void *d_wimg = nullptr;       // K5 filter TMEM image [n_sets][2][nks][2][2b + 256] x 16 B
-  void *d_win5 = nullptr;       // K5 class-sorted window table (device copy, read when it has > 64 entries)
   int32_t last_kernel = -1;     // kernel launched by the most recent ce_estimate
   bool even_starts = true;      // all window starts even (K4 TMA alignment)
   int32_t *d_flag = nullptr;    // [1] build error flag
@@ -127,8 +124,6 @@ void release(ce_handle *h) {
   cudaFree(h->d_Wt);
   cudaFree(h->d_bank);
   cudaFree(h->d_bank16);
-  cudaFree(h->d_wimg);
-  cudaFree(h->d_win5);
   cudaFree(h->d_flag);
   cudaFreeHost(h->h_flag);
   cudaFree(h->d_stage);
@@ -165,7 +160,7 @@ extern "C" {
 
 const char *ce_version(void) {
   return "libce 0.4 sm_100a (K1 fp64 Levinson/Schur + refinement + Gohberg-Semencul/Trench, K2 fp32 simt, K3 tcgen05 "
-         "tf32x3, K4 tcgen05 bf16x3 + TMA, K5 tcgen05 cta-pair bf16x3 with the filter resident in TMEM)";
+         "tf32x3, K4 tcgen05 bf16x3 + TMA)";
 }
 
 const char *ce_status_string(int status) {
@@ -268,19 +263,6 @@ int ce_init(const ce_params *p, ce_handle **out) {
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank, 2 * h->bank_plane * sizeof(float)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank16, 2 * h->bank16_plane * sizeof(uint16_t)));
-  std::vector<uint8_t> win5;
-  if (e == cudaSuccess && h->tf32_ok && h->even_starts && ce::pair_supported(b)) {
-    ce::ContractArgs ga;
-    ga.geo_host = h->geo_tc.data();
-    ga.n_win = int32_t(h->geo_tc.size());
-    ga.b = b;
-    ga.N = N;
-    if (ce::pair_window_table(ga, &win5)) {
-      chk(cudaMalloc(&h->d_wimg, ce::pair_wimg_elems(b, S) * 16));
-      chk(cudaMalloc(&h->d_win5, win5.size()));
-      h->pair_ok = true;
-    }
-  }
   chk(cudaMalloc(&h->d_flag, sizeof(int32_t)));
   chk(cudaMallocHost(&h->h_flag, sizeof(int32_t)));
   if (e == cudaSuccess) {
@@ -288,7 +270,6 @@ int ce_init(const ce_params *p, ce_handle **out) {
     chk(cudaMemcpy(h->d_sigma2, p->sigma2, size_t(S) * sizeof(double), cudaMemcpyHostToDevice));
     chk(cudaMemcpy(h->d_geo, geo.data(), geo.size() * sizeof(ce::Window), cudaMemcpyHostToDevice));
     chk(cudaMemcpy(h->d_geo_tc, h->geo_tc.data(), h->geo_tc.size() * sizeof(ce::Window), cudaMemcpyHostToDevice));
-    if (h->pair_ok) chk(cudaMemcpy(h->d_win5, win5.data(), win5.size(), cudaMemcpyHostToDevice));
   }
   if (e != cudaSuccess) {
     int st = cuda_fail(e, "ce_init: device allocation/copy");
@@ -313,14 +294,12 @@ int ce_free(ce_handle *h) {
 int ce_set_kernel(ce_handle *h, int32_t kernel) {
   if (h == nullptr) return fail(CE_EINVAL, "ce_set_kernel: NULL handle");
   if (kernel != CE_KERNEL_AUTO && kernel != CE_KERNEL_SIMT && kernel != CE_KERNEL_TF32X3 &&
-      kernel != CE_KERNEL_BF16X3 && kernel != CE_KERNEL_BF16X3_PAIR)
+      kernel != CE_KERNEL_BF16X3)
     return fail(CE_EINVAL, "ce_set_kernel: unknown kernel");
-  if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->tf32_ok)
+  if ((kernel == CE_KERNEL_TF32X3 || kernel == CE_KERNEL_BF16X3) && !h->tf32_ok)
     return fail(CE_EINVAL, "ce_set_kernel: tensor-core filter banks do not fit for this b");
-  if ((kernel == CE_KERNEL_BF16X3 || kernel == CE_KERNEL_BF16X3_PAIR) && !h->even_starts)
-    return fail(CE_EINVAL, "ce_set_kernel: BF16X3 / BF16X3_PAIR need every window start a_w even (16-byte TMA boxes)");
-  if (kernel == CE_KERNEL_BF16X3_PAIR && !h->pair_ok)
-    return fail(CE_EINVAL, "ce_set_kernel: BF16X3_PAIR holds the filter in TMEM: needs b <= 208");
+  if (kernel == CE_KERNEL_BF16X3 && !h->even_starts)
+    return fail(CE_EINVAL, "ce_set_kernel: BF16X3 needs every window start a_w even (16-byte TMA boxes)");
   h->kernel = kernel;
   return CE_OK;
 }
@@ -359,9 +338,6 @@ int ce_build_filters(ce_handle *h, void *stream) {
                                        &h->launches),
             "ce_build_filters: bf16 bank launch");
   }
-  if (h->pair_ok)
-    CE_CUDA(ce::launch_build_wimg(h->d_W, h->b, h->n_sets, h->d_wimg, st, &h->launches),
-            "ce_build_filters: K5 filter image launch");
   CE_CUDA(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st),
           "ce_build_filters: flag copy");
   CE_CUDA(cudaStreamSynchronize(st), "ce_build_filters: synchronize");
@@ -409,13 +385,8 @@ static int launch_contract(ce_handle *h, const float2 *y, const float2 *x, float
     k = !h->tf32_ok ? CE_KERNEL_SIMT : (ce::bf16x3_launchable(a) ? CE_KERNEL_BF16X3 : CE_KERNEL_TF32X3);
   if (k == CE_KERNEL_BF16X3 && !ce::bf16x3_launchable(a))
     return fail(CE_EINVAL, "ce_estimate: BF16X3 needs K <= 32, even N, even window starts, 16-byte aligned y/x");
-  if (k == CE_KERNEL_BF16X3_PAIR && !(h->pair_ok && ce::pair_launchable(a)))
-    return fail(CE_EINVAL, "ce_estimate: BF16X3_PAIR needs K <= 32, even N, even window starts, 16-byte aligned y/x "
-                           "and b <= 208");
   cudaError_t e;
-  if (k == CE_KERNEL_BF16X3_PAIR)
-    e = ce::launch_contract_pair(a, h->d_wimg, h->d_win5, st, &h->launches);
-  else if (k == CE_KERNEL_BF16X3)
+  if (k == CE_KERNEL_BF16X3)
     e = ce::launch_contract_bf16x3(a, h->d_bank16, h->d_bank16 + h->bank16_plane, st, &h->launches);
   else if (k == CE_KERNEL_TF32X3)
     e = ce::launch_contract_tf32x3(a, h->d_bank, h->d_bank + h->bank_plane, st, &h->launches);

@@ -61,15 +61,6 @@ cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets,
 cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches);
 
-// K5: CTA pair (cta_group::2) with the filter stationary in TMEM (A operand) and the LS tile as the B operand.
-bool pair_supported(int32_t b);                           // the filter's TMEM image fits beside two accumulators
-size_t pair_wimg_elems(int32_t b, int32_t n_sets);        // 16-byte elements of the filter TMEM image
-cudaError_t launch_build_wimg(const float2 *d_W, int32_t b, int32_t n_sets, void *wimg, cudaStream_t stream,
-                              int64_t *launches);
-bool pair_window_table(const ContractArgs &a, std::vector<uint8_t> *bytes);   // class-sorted table (geometry only)
-bool pair_launchable(const ContractArgs &a);
-cudaError_t launch_contract_pair(const ContractArgs &a, const void *wimg, const void *win_dev, cudaStream_t stream,
-                                 int64_t *launches);
 
 // K8: the statistics estimator's lag correlation (banded Gram matrix) on tcgen05; adds into K7's accumulator.
 bool gram_launchable(const float2 *y, int32_t K, int32_t N, int32_t D);

@@ -9,7 +9,6 @@
 // B_r^T rows 2i / 2i+1 = (Re W_ij, -Im W_ij) / (Im W_ij, Re W_ij)).
 //
 // Work unit: a tile = (instance t, window w, 128-column block ct); one CTA per SM walks its tiles.
-// (The CTA-pair variant, cta_group::2 with the filter bank resident, is K5.)
 //
 // Pipeline (persistent, one CTA per SM, 480 threads):
 //   warp 12   : raw producer -- 2D TMA of the raw y box [128 rows x 16 complex] and the pilot box
@@ -89,7 +88,6 @@ static_assert(K4_SMEM <= 232448, "K4 shared memory");
 
 struct K4Params {
   float2 *h;
-  const float2 *y;           // raw y (L2 prefetch by the epilogue warps, lsu_pf)
   const uint16_t *bank_hi;   // bf16 [n_sets][nkc][NR][32] swizzled SW64 rows
   const uint16_t *bank_lo;
   const Window *geo;         // device window table (read only when n_win > MAXW_PARAM)
@@ -101,8 +99,6 @@ struct K4Params {
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
   int l2_hint;               // bit 0: y loads evict_first; 1: h TMA stores evict_first; 2: x loads evict_last;
                              // 3: filter-bank loads evict_last (experiments beyond bit 0)
-  int pf_dist;               // raw chunks prefetched into L2 ahead of their tensor load (0: none)
-  int lsu_pf;                // epilogue warps prefetch y into L2 by prefetch.global.L2: bit 0 first tile, bit 1 next tile
   Window geo_s[MAXW_PARAM];
 };
 
@@ -317,20 +313,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // ---------------------------------------------------------------- raw producer (TMA)
     if (lane == 0) {
       const uint32_t xbytes = uint32_t(xbytes0);
-      // L2 prefetch of the y box pf_dist chunks ahead of its tensor load (the ring's shared memory bounds the loads in
-      // flight; prefetches are not bounded by it).  Chunk j of this CTA is (tile blockIdx.x + (j / nkc) * grid, j % nkc).
-      int pf_next = 0;
-      auto prefetch_upto = [&](int j_end) {
-        for (; pf_next < j_end; ++pf_next) {
-          const int g = blockIdx.x + (pf_next / nkc0) * int(gridDim.x);
-          if (g >= p.n_tiles) {
-            pf_next = 1 << 30;
-            return;
-          }
-          const Tile4 tp = g == int(blockIdx.x) ? ti0 : decode4(p, g);
-          tma_prefetch_2d(&tmy, 2 * (tp.a + (pf_next % nkc0) * CK), tp.t * cols0 + tp.ct * TM);
-        }
-      };
       int it = 0;
       for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
         const Tile4 ti = g == int(blockIdx.x) ? ti0 : decode4(p, g);
@@ -340,7 +322,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         const int row0 = g == int(blockIdx.x) ? row0_0 : ti.t * cols0 + ti.ct * TM;
         for (int kc = 0; kc < nkc0; ++kc, ++it) {
           const int s = it % S_RAW;
-          if (p.pf_dist > 0) prefetch_upto(it + p.pf_dist);
           mbar_wait(&raw_empty[s], ((it / S_RAW) & 1) ^ 1);
 #ifdef CE_K4_TRACE
           if (it == 0) c_w0 = clock64();
@@ -442,23 +423,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // TMEM -> registers (16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row)
     // -> direct 8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes.
     const int q = warp & 3;
-    // L2 prefetch of a tile's y rows through the LSU (one row per epilogue thread): raises the DRAM requests in
-    // flight beyond the raw ring's shared memory without costing TMA-engine time
-    auto pf_tile = [&](int g) {
-      if (g >= p.n_tiles) return;
-      const Tile4 tp = decode4(p, g);
-      const int c = tp.ct * TM + q * 32 + lane;
-      if (c >= p.cols) return;
-      const char *row = reinterpret_cast<const char *>(p.y + (size_t(tp.t) * p.cols + c) * p.N + tp.a);
-      const char *end = row + size_t(p.b) * 8;
-      for (const char *a = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(row) & ~uintptr_t(127)); a < end;
-           a += 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    };
-    if (p.lsu_pf & 1) pf_tile(blockIdx.x);
     int lt = 0;
     for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
-      if (p.lsu_pf & 2) pf_tile(g + int(gridDim.x));
       const Tile4 ti = decode4(p, g);
       const bool set_ok = tile_set(p, ti.t) >= 0;
       const bool last = p.tma_last && g + int(gridDim.x) >= p.n_tiles;
@@ -695,11 +661,6 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   // pilots and filter-bank chunks (re-read by every column tile) evict_last: config 3 -0.5%, config 4 -0.8% (same
   // box, two repetitions), configs 5-6 equal
   p.l2_hint = env_hint >= 0 ? env_hint : ((tiles <= (long long)di->num_sms && disjoint ? 1 : 0) | 4 | 8);
-  static const int env_pf = getenv("CE_K4_PF") ? atoi(getenv("CE_K4_PF")) : 0;   // experiments
-  p.pf_dist = env_pf;
-  static const int env_lpf = getenv("CE_K4_LSUPF") ? atoi(getenv("CE_K4_LSUPF")) : 0;   // experiments
-  p.lsu_pf = env_lpf;
-  p.y = a.y;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
   cfg.blockDim = dim3(K4_THREADS);

@@ -122,13 +122,6 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const void *tmap, int c0,
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-// L2 prefetch of a 2-D TMA box (no shared memory, no completion): raises the DRAM requests in flight beyond what the
-// shared-memory ring holds; the later tensor load of the same box then hits L2.
-__device__ __forceinline__ void tma_prefetch_2d(const void *tmap, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(tmap)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));

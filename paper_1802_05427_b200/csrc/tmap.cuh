@@ -1,4 +1,4 @@
-// Host-side TMA tensor-map helpers shared by the tcgen05 contraction kernels (K4, K5).
+// Host-side TMA tensor-map helpers shared by the tcgen05 contraction kernels (K4, K8).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>

@@ -1,7 +1,7 @@
 """Every path the tensor-core kernels serve, on geometries where they are the launched kernel.
 
-K4 (CE_KERNEL_BF16X3) and K5 (CE_KERNEL_BF16X3_PAIR) need even window starts, so the config-2 checks of
-test_gpu_parity.py (odd starts) never reach them.  Here, on the config-3 and config-4 geometries (the paper-scale
+K4 (CE_KERNEL_BF16X3, the AUTO kernel) needs even window starts, so the config-2 checks of test_gpu_parity.py
+(odd starts) never reach it.  Here, on the config-3 and config-4 geometries (the paper-scale
 slot and the batched frame, Eq. 12 per block with the Table II edge clamping):
 - shard invariance through offset device pointers (the multi-GPU design rests on it: the filters
   "bear no relation with the receiving antennas"), G = 2 / 4 / 8 antenna shards bitwise equal to the full call;
@@ -23,7 +23,7 @@ from workload import CONFIGS
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TC_KERNELS = [3, 4]     # CE_KERNEL_BF16X3 (K4), CE_KERNEL_BF16X3_PAIR (K5)
+TC_KERNELS = [3]        # CE_KERNEL_BF16X3 (K4); AUTO selects it on every geometry below
 
 
 def _ce():
