@@ -248,16 +248,25 @@ __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ 
     }
   }
   __syncthreads();
-  // phase 3: coalesced rows out (3W: zero-order hold on the way out)
+  // phase 3: coalesced rows out (3W: zero-order hold on the way out).  12W: threads 0 .. 8 SS - 1 each own one
+  // output phase q = tid % SS and group offset tid / SS, and stride by 8 groups: tone k = SS g + q = tid + 8 SS i,
+  // so every pass writes 8 SS consecutive tones with no division in the loop
   constexpr int step = SS / GG;
-  for (int r = 0; r < rows; ++r) {
-    float2 *hr = h + ((row0 + r) * g.n_ue + s) * N;
-    const float2 *o = outs + r * per_row;
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      if (MODE == 0)
-        hr[k] = o[(k % SS) * (K + 1) + k / SS];
-      else
-        hr[k] = o[k >= s ? (k - s) / step : 0];
+  if (MODE == 0) {
+    constexpr int GS = 8;
+    if (threadIdx.x < GS * SS) {
+      const int q = threadIdx.x % SS, go = threadIdx.x / SS;
+      for (int r = 0; r < rows; ++r) {
+        float2 *hr = h + ((row0 + r) * g.n_ue + s) * N + threadIdx.x;
+        const float2 *o = outs + r * per_row + q * (K + 1);
+        for (int gq = go, i = 0; gq < K; gq += GS, i += GS * SS) hr[i] = o[gq];
+      }
+    }
+  } else {
+    for (int r = 0; r < rows; ++r) {
+      float2 *hr = h + ((row0 + r) * g.n_ue + s) * N;
+      const float2 *o = outs + r * per_row;
+      for (int k = threadIdx.x; k < N; k += blockDim.x) hr[k] = o[k >= s ? (k - s) / step : 0];
     }
   }
 }
@@ -293,15 +302,16 @@ __global__ void __launch_bounds__(192) k6_estimate_poly(const float2 *__restrict
   const int s = (threadIdx.x / SS) % n_ue;
   const int r = threadIdx.x / (SS * n_ue);
   const bool active = r < rows;
-  // interior weight row W_s(ml)[q][.] as FFMA2 operand pairs
-  uint64_t wab[GG], wba[GG];
+  // interior weight row W_s(ml)[q][.] as packed (re, im) FFMA2 operands.  Each output accumulates P = sum l.re w and
+  // Q = sum l.im w (two independent chains, the LS component as FFMA2's broadcast scalar operand), then
+  // w l = (P.re - Q.im, P.im + Q.re): one packed weight per tap, no (-im, re) copies
+  uint64_t wab[GG];
   {
     const float2 *w = W + ((size_t(s) * GG + ml) * SS + q) * GG;
 #pragma unroll
     for (int j = 0; j < GG; ++j) {
       const float2 wv = __ldg(w + j);
       wab[j] = pk2(wv.x, wv.y);
-      wba[j] = pk2(-wv.y, wv.x);
     }
   }
   __syncthreads();
@@ -314,26 +324,26 @@ __global__ void __launch_bounds__(192) k6_estimate_poly(const float2 *__restrict
         const int a = min(max(gq - ml, 0), K - GG);
         const int typ = gq - a;
         const float2 *l = lr + SS * a;
-        uint64_t acc0 = 0ull, acc1 = 0ull;
+        uint64_t acc0 = 0ull, acc1 = 0ull;                        // P, Q
         if (typ == ml) {
 #pragma unroll
-          for (int j = 0; j < GG; j += 2) {
-            const float2 l0 = l[SS * j], l1 = l[SS * (j + 1)];
-            acc0 = fma2(pk2(l0.x, l0.x), wab[j], fma2(pk2(l0.y, l0.y), wba[j], acc0));
-            acc1 = fma2(pk2(l1.x, l1.x), wab[j + 1], fma2(pk2(l1.y, l1.y), wba[j + 1], acc1));
+          for (int j = 0; j < GG; ++j) {
+            const float2 lv = l[SS * j];
+            acc0 = fma2(pk2(lv.x, lv.x), wab[j], acc0);
+            acc1 = fma2(pk2(lv.y, lv.y), wab[j], acc1);
           }
         } else {                                                  // edge group: its own weight type (L1-cached)
           const float2 *w = W + ((size_t(s) * GG + typ) * SS + q) * GG;
 #pragma unroll
-          for (int j = 0; j < GG; j += 2) {
-            const float2 l0 = l[SS * j], l1 = l[SS * (j + 1)];
-            const float2 w0 = __ldg(w + j), w1 = __ldg(w + j + 1);
-            acc0 = fma2(pk2(l0.x, l0.x), pk2(w0.x, w0.y), fma2(pk2(l0.y, l0.y), pk2(-w0.y, w0.x), acc0));
-            acc1 = fma2(pk2(l1.x, l1.x), pk2(w1.x, w1.y), fma2(pk2(l1.y, l1.y), pk2(-w1.y, w1.x), acc1));
+          for (int j = 0; j < GG; ++j) {
+            const float2 lv = l[SS * j], wv = __ldg(w + j);
+            const uint64_t wj = pk2(wv.x, wv.y);
+            acc0 = fma2(pk2(lv.x, lv.x), wj, acc0);
+            acc1 = fma2(pk2(lv.y, lv.y), wj, acc1);
           }
         }
-        const float2 o0 = upk2(acc0), o1 = upk2(acc1);
-        sr[(gq - g0) * SS + q] = make_float2(o0.x + o1.x, o0.y + o1.y);
+        const float2 P = upk2(acc0), Q = upk2(acc1);
+        sr[(gq - g0) * SS + q] = make_float2(P.x - Q.y, P.y + Q.x);
       }
     }
     __syncthreads();
