@@ -271,96 +271,6 @@ __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ 
   }
 }
 
-// K6c -- the paper's 12W (full mode, S = G = 12) as a polyphase filter over the pilot axis: one thread per (row, UE
-// s, output phase q) computes the outputs S g + q of every group g of its row (12 outputs per group
-// from the group's 12 pilots; Table II: interior groups g in [ml, K - G + ml] all use weight type
-// W(ml) on pilots g - ml .. g - ml + G - 1, edge groups the clamped windows).  The interior weight row W_s(ml)[q][.]
-// sits in registers as packed (re, im) / (-im, re) pairs; every output is 12 complex MACs as FFMA2 in two
-// independent chains (even / odd taps).  The CTA's rows' LS values (every tone: tone k is UE k mod S's pilot) are
-// formed once into shared memory; outputs are staged per chunk of GC groups and leave as contiguous float4 rows.
-// One CTA per (instance, block of rpc rows); rows = T*M received rows; threads = rpc * n_ue * S.
-constexpr int K6C_GC = 20;
-template <int SS, int GG>
-__global__ void __launch_bounds__(192) k6_estimate_poly(const float2 *__restrict__ y, const float2 *__restrict__ x,
-                                                        const float2 *__restrict__ W, float2 *__restrict__ h,
-                                                        int rows_total, int M, int rpc, CombGeo g) {
-  extern __shared__ float4 sm6c[];
-  const int N = g.N, K = g.K, n_ue = g.n_ue, ml = g.ml;
-  float2 *ls = reinterpret_cast<float2 *>(sm6c);                  // [rpc][N]
-  float2 *stg = ls + size_t(rpc) * N;                             // [rpc][n_ue][GC * SS]
-  const int row0 = blockIdx.x * rpc;
-  const int rows = min(rpc, rows_total - row0);
-  // LS of every tone of the block's rows: y / x = y conj(x) / |x|^2 (Eq. 9)
-  for (int e = threadIdx.x; e < rows * N; e += blockDim.x) {
-    const int r = e / N, k = e - r * N;
-    const int t = (row0 + r) / M;
-    const float2 yv = y[size_t(row0 + r) * N + k], xv = __ldg(x + size_t(t) * N + k);
-    const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
-    ls[e] = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
-  }
-  const int q = threadIdx.x % SS;
-  const int s = (threadIdx.x / SS) % n_ue;
-  const int r = threadIdx.x / (SS * n_ue);
-  const bool active = r < rows;
-  // interior weight row W_s(ml)[q][.] as packed (re, im) FFMA2 operands.  Each output accumulates P = sum l.re w and
-  // Q = sum l.im w (two independent chains, the LS component as FFMA2's broadcast scalar operand), then
-  // w l = (P.re - Q.im, P.im + Q.re): one packed weight per tap, no (-im, re) copies
-  uint64_t wab[GG];
-  {
-    const float2 *w = W + ((size_t(s) * GG + ml) * SS + q) * GG;
-#pragma unroll
-    for (int j = 0; j < GG; ++j) {
-      const float2 wv = __ldg(w + j);
-      wab[j] = pk2(wv.x, wv.y);
-    }
-  }
-  __syncthreads();
-  const float2 *lr = ls + size_t(r) * N + s;                      // this (row, UE)'s pilots: lr[SS p]
-  float2 *sr = stg + size_t(r * n_ue + s) * (K6C_GC * SS);
-  for (int g0 = 0; g0 < K; g0 += K6C_GC) {
-    const int g1 = min(K, g0 + K6C_GC);
-    if (active) {
-      for (int gq = g0; gq < g1; ++gq) {
-        const int a = min(max(gq - ml, 0), K - GG);
-        const int typ = gq - a;
-        const float2 *l = lr + SS * a;
-        uint64_t acc0 = 0ull, acc1 = 0ull;                        // P, Q
-        if (typ == ml) {
-#pragma unroll
-          for (int j = 0; j < GG; ++j) {
-            const float2 lv = l[SS * j];
-            acc0 = fma2(pk2(lv.x, lv.x), wab[j], acc0);
-            acc1 = fma2(pk2(lv.y, lv.y), wab[j], acc1);
-          }
-        } else {                                                  // edge group: its own weight type (L1-cached)
-          const float2 *w = W + ((size_t(s) * GG + typ) * SS + q) * GG;
-#pragma unroll
-          for (int j = 0; j < GG; ++j) {
-            const float2 lv = l[SS * j], wv = __ldg(w + j);
-            const uint64_t wj = pk2(wv.x, wv.y);
-            acc0 = fma2(pk2(lv.x, lv.x), wj, acc0);
-            acc1 = fma2(pk2(lv.y, lv.y), wj, acc1);
-          }
-        }
-        const float2 P = upk2(acc0), Q = upk2(acc1);
-        sr[(gq - g0) * SS + q] = make_float2(P.x - Q.y, P.y + Q.x);
-      }
-    }
-    __syncthreads();
-    // contiguous output segments [SS g0, SS g1) of every (row, UE) row of h, as float4 (two complex) stores
-    const int seg = (g1 - g0) * SS;                               // even (SS even)
-    const int per = seg / 2;
-    for (int e = threadIdx.x; e < rows * n_ue * per; e += blockDim.x) {
-      const int rs = e / per, i = e - rs * per;
-      const float4 v = reinterpret_cast<const float4 *>(stg + size_t(rs) * (K6C_GC * SS))[i];
-      const int rr = rs / n_ue, ss = rs - rr * n_ue;
-      float2 *hp = h + (size_t(row0 + rr) * n_ue + ss) * N + SS * g0;
-      reinterpret_cast<float4 *>(hp)[i] = v;
-    }
-    __syncthreads();
-  }
-}
-
 }  // namespace
 }  // namespace ce
 
@@ -485,22 +395,7 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
   const size_t smem_g = (size_t(g.G) * g.n_out * g.G + size_t(ce::RB) * g.K +
                          size_t(ce::RB) * (g.mode == CE_COMB_FULL ? size_t(g.n_out) * (g.K + 1) : size_t(g.K) * g.G)) *
                         sizeof(float2);
-  static const int env_k6 = getenv("CE_K6_POLY") ? atoi(getenv("CE_K6_POLY")) : 0;   // experiments (K6c: slower so far)
-  const bool poly = env_k6 != 0 && g.mode == CE_COMB_FULL && g.S == 12 && g.G == 12 &&
-                    (reinterpret_cast<uintptr_t>(d_h) & 15) == 0 && (g.N % 2) == 0;
-  if (poly) {
-    // rows per CTA: ~12 threads' worth of (UE, phase) work per row, shared memory for the LS rows <= 48 KB
-    int rpc = std::max(1, 12 / g.n_ue);
-    while (rpc > 1 && size_t(rpc) * g.N * sizeof(float2) > 48 * 1024) --rpc;
-    const long long rows_total = (long long)T * M;
-    const long long blocks = (rows_total + rpc - 1) / rpc;
-    if (blocks > 0x7fffffffLL) return cfail(CE_EINVAL, "ce_comb_estimate: too many rows");
-    const int threads = (rpc * g.n_ue * 12 + 31) / 32 * 32;
-    const size_t smem = (size_t(rpc) * g.N + size_t(rpc) * g.n_ue * ce::K6C_GC * 12) * sizeof(float2);
-    cudaError_t e = ce::smem_opt_in((const void *)ce::k6_estimate_poly<12, 12>, smem);
-    if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: smem attribute");
-    ce::k6_estimate_poly<12, 12><<<unsigned(blocks), threads, smem, st>>>(yp, xp, h->d_W, hp, int(rows_total), M, rpc, g);
-  } else if (spec && smem_g <= 200 * 1024) {
+  if (spec && smem_g <= 200 * 1024) {
     const size_t n_mb = (size_t(M) + ce::RB - 1) / ce::RB;
     const size_t blocks = size_t(T) * n_mb * g.n_ue;
     if (blocks > 0x7fffffffULL) return cfail(CE_EINVAL, "ce_comb_estimate: too many rows");
