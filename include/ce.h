@@ -120,6 +120,19 @@ int ce_estimate(ce_handle *h, const void *d_y, const void *d_x, void *d_h,
 int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void *h_host,
                      int32_t T, int32_t M, int32_t K, const int32_t *set_of_instance, void *stream);
 
+/* Asynchronous form of ce_estimate_host: the same copies and kernels, ordered after the work enqueued on `stream`
+ * before this call, on the handle's internal streams; the call returns once everything is enqueued, and `stream`
+ * does NOT wait for it -- call ce_estimate_host_wait (or synchronise the device) before reading h_host.  y_host,
+ * x_host, set_of_instance and h_host must stay valid (and h_host unread) until then.  The handle alternates two
+ * device staging slots, so consecutive calls overlap (one call's device->host copies with the next call's
+ * host->device copies); a call on a slot waits on the device for the previous user of that slot.  Pinned host
+ * memory is required for the copies to be asynchronous.  Same validation and errors as ce_estimate_host. */
+int ce_estimate_host_async(ce_handle *h, const void *y_host, const void *x_host, void *h_host,
+                           int32_t T, int32_t M, int32_t K, const int32_t *set_of_instance, void *stream);
+
+/* Make `stream` wait (on the device) for every ce_estimate_host_async call enqueued on the handle so far. */
+int ce_estimate_host_wait(ce_handle *h, void *stream);
+
 /* Free W, workspace, staging buffers and the handle.  NULL is allowed (no-op). */
 int ce_free(ce_handle *h);
 

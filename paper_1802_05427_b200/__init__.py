@@ -27,6 +27,8 @@ from .ce import (  # noqa: F401
     ce_comb_init,
     ce_estimate,
     ce_estimate_host,
+    ce_estimate_host_async,
+    ce_estimate_host_wait,
     ce_free,
     ce_get_filters,
     ce_init,

@@ -26,7 +26,9 @@ CE_OK, CE_EINVAL, CE_ENOMEM, CE_ECUDA, CE_ENOTPD, CE_ESTATE, CE_ENODEV = 0, -1, 
 CE_KERNEL_AUTO, CE_KERNEL_SIMT, CE_KERNEL_TF32X3, CE_KERNEL_BF16X3 = 0, 1, 2, 3   # 4 (K5) retired: CE_EINVAL
 
 # every function declared in include/ce.h (tests check the .so exports all of them)
-EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_estimate_host_async",
+            "ce_estimate_host_wait", "ce_free",
+            "ce_set_kernel",
             "ce_selected_kernel",
             "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
             "ce_version", "ce_comb_init", "ce_comb_build_filters", "ce_comb_estimate", "ce_comb_get_filters",
@@ -57,6 +59,8 @@ lib.ce_stats_estimate.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int32,
 lib.ce_build_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]
 lib.ce_estimate_host.argtypes = lib.ce_estimate.argtypes
+lib.ce_estimate_host_async.argtypes = lib.ce_estimate.argtypes
+lib.ce_estimate_host_wait.argtypes = [c_void_p, c_void_p]
 lib.ce_free.argtypes = [c_void_p]
 lib.ce_set_kernel.argtypes = [c_void_p, c_int32]
 lib.ce_selected_kernel.argtypes = [c_void_p, POINTER(c_int32)]
@@ -69,7 +73,9 @@ lib.ce_last_error.argtypes = []
 lib.ce_last_error.restype = c_char_p
 lib.ce_version.argtypes = []
 lib.ce_version.restype = c_char_p
-for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_free", "ce_set_kernel",
+for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce_estimate_host_async",
+           "ce_estimate_host_wait", "ce_free",
+           "ce_set_kernel",
            "ce_selected_kernel",
            "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_comb_init", "ce_comb_build_filters",
            "ce_comb_estimate", "ce_comb_get_filters", "ce_comb_launch_count", "ce_comb_free"):
@@ -148,6 +154,16 @@ def ce_estimate_host(h: int, y_ptr: int, x_ptr: int, h_ptr: int, T: int, M: int,
                      stream: int = 0) -> None:
     _check(lib.ce_estimate_host(h, c_void_p(y_ptr), c_void_p(x_ptr), c_void_p(h_ptr), T, M, K,
                                 c_void_p(soi_ptr or None), c_void_p(stream)), "ce_estimate_host")
+
+
+def ce_estimate_host_async(h: int, y_ptr: int, x_ptr: int, h_ptr: int, T: int, M: int, K: int, soi_ptr: int = 0,
+                           stream: int = 0) -> None:
+    _check(lib.ce_estimate_host_async(h, c_void_p(y_ptr), c_void_p(x_ptr), c_void_p(h_ptr), T, M, K,
+                                      c_void_p(soi_ptr or None), c_void_p(stream)), "ce_estimate_host_async")
+
+
+def ce_estimate_host_wait(h: int, stream: int = 0) -> None:
+    _check(lib.ce_estimate_host_wait(h, c_void_p(stream)), "ce_estimate_host_wait")
 
 
 def ce_free(h: int) -> None:
@@ -229,11 +245,13 @@ class ChannelEstimator:
         ce_estimate(self.handle, y.data_ptr(), x.data_ptr(), out.data_ptr(), T, M, K, soi, _stream_ptr(stream))
         return out
 
-    def estimate_host(self, y, x, out=None, set_of_instance=None, stream=None):
+    def estimate_host(self, y, x, out=None, set_of_instance=None, stream=None, sync=True):
         """End-to-end path through ce_estimate_host: host (NumPy or pinned torch) buffers in and out.
 
         ce_estimate_host copies T*M*K*N elements to and from the raw host pointers, so every shape is checked
-        here before the call (a mismatch would over-read y / x or over-write out)."""
+        here before the call (a mismatch would over-read y / x or over-write out).  sync=False uses
+        ce_estimate_host_async: the call returns once enqueued; the host buffers (pinned) must stay alive and out
+        unread until host_wait(stream) has been called and the stream has reached that point."""
         if len(tuple(y.shape)) != 4:
             raise ValueError(f"y must be [T][M][K][N], got shape {tuple(y.shape)}")
         T, M, K, N = (int(v) for v in y.shape)
@@ -249,9 +267,15 @@ class ChannelEstimator:
             if set_of_instance.shape[0] < T:
                 raise ValueError(f"set_of_instance needs >= T = {T} entries, got {set_of_instance.shape[0]}")
             soi_ptr = set_of_instance.ctypes.data
-        ce_estimate_host(self.handle, _host_ptr(y), _host_ptr(x), _host_ptr(out), T, M, K, soi_ptr,
-                         _stream_ptr(stream))
+        fn = ce_estimate_host if sync else ce_estimate_host_async
+        fn(self.handle, _host_ptr(y), _host_ptr(x), _host_ptr(out), T, M, K, soi_ptr, _stream_ptr(stream))
+        if not sync:                                       # keep the host buffers of the calls in flight alive
+            self._inflight = (getattr(self, "_inflight", ()) + ((y, x, out, set_of_instance),))[-2:]
         return out
+
+    def host_wait(self, stream=None) -> None:
+        """Make `stream` wait for every estimate_host(..., sync=False) call enqueued so far."""
+        ce_estimate_host_wait(self.handle, _stream_ptr(stream))
 
     def selected_kernel(self) -> int:
         return ce_selected_kernel(self.handle)

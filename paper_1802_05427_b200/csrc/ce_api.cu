@@ -82,9 +82,12 @@ struct ce_handle {
   bool even_starts = true;      // all window starts even (K4 TMA alignment)
   int32_t *d_flag = nullptr;    // [1] build error flag
   int32_t *h_flag = nullptr;    // pinned mirror
-  // host-buffer path (grown on demand)
-  void *d_stage = nullptr;
-  size_t stage_bytes = 0;
+  // host-buffer path: two staging slots (grown on demand) so that two calls can be in flight; a call on slot s
+  // waits for ev_slot_free[s], recorded after the last D2H copy of the previous call that used the slot
+  void *d_stage[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
+  int next_slot = 0;
+  cudaEvent_t ev_slot_free[2] = {nullptr, nullptr};
   // host-buffer pipeline: streams[0] H2D copies, [1] kernels, [2] D2H copies; per-chunk events
   static constexpr int MAX_CHUNKS = 64;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
@@ -126,7 +129,10 @@ void release(ce_handle *h) {
   cudaFree(h->d_bank16);
   cudaFree(h->d_flag);
   cudaFreeHost(h->h_flag);
-  cudaFree(h->d_stage);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(h->d_stage[i]);
+    if (h->ev_slot_free[i]) cudaEventDestroy(h->ev_slot_free[i]);
+  }
   for (auto &s : h->streams)
     if (s) cudaStreamDestroy(s);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
@@ -263,6 +269,7 @@ int ce_init(const ce_params *p, ce_handle **out) {
   chk(cudaMalloc(&h->d_Wt, size_t(S) * b * b * sizeof(float2)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank, 2 * h->bank_plane * sizeof(float)));
   if (h->tf32_ok) chk(cudaMalloc(&h->d_bank16, 2 * h->bank16_plane * sizeof(uint16_t)));
+
   chk(cudaMalloc(&h->d_flag, sizeof(int32_t)));
   chk(cudaMallocHost(&h->h_flag, sizeof(int32_t)));
   if (e == cudaSuccess) {
@@ -416,53 +423,60 @@ int ce_estimate(ce_handle *h, const void *d_y, const void *d_x, void *d_h, int32
                          static_cast<float2 *>(d_h), T, M, K, d_set_of_instance, static_cast<cudaStream_t>(stream));
 }
 
-int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void *h_host, int32_t T, int32_t M,
-                     int32_t K, const int32_t *set_of_instance, void *stream) {
-  if (h == nullptr) return fail(CE_EINVAL, "ce_estimate_host: NULL handle");
-  if (!h->built) return fail(CE_ESTATE, "ce_estimate_host: call ce_build_filters first");
+static int estimate_host_impl(ce_handle *h, const void *y_host, const void *x_host, void *h_host, int32_t T,
+                              int32_t M, int32_t K, const int32_t *set_of_instance, void *stream, bool sync) {
+  const char *who = sync ? "ce_estimate_host" : "ce_estimate_host_async";
+  if (h == nullptr) return fail(CE_EINVAL, std::string(who) + ": NULL handle");
+  if (!h->built) return fail(CE_ESTATE, std::string(who) + ": call ce_build_filters first");
   if (y_host == nullptr || x_host == nullptr || h_host == nullptr)
-    return fail(CE_EINVAL, "ce_estimate_host: NULL pointer");
+    return fail(CE_EINVAL, std::string(who) + ": NULL pointer");
   int st = check_sizes(h, T, M, K);
   if (st != CE_OK) return st;
   const size_t N = size_t(h->N);
   const size_t ny = size_t(T) * M * K * N * sizeof(float2);
   const size_t nx = size_t(T) * K * N * sizeof(float2);
   if (overlaps(h_host, ny, y_host, ny) || overlaps(h_host, ny, x_host, nx))
-    return fail(CE_EINVAL, "ce_estimate_host: output aliases an input");
+    return fail(CE_EINVAL, std::string(who) + ": output aliases an input");
   if (set_of_instance)
     for (int32_t t = 0; t < T; ++t)
       if (set_of_instance[t] < 0 || set_of_instance[t] >= h->n_sets)
-        return fail(CE_EINVAL, "ce_estimate_host: set_of_instance out of range");
+        return fail(CE_EINVAL, std::string(who) + ": set_of_instance out of range");
   DeviceGuard g(h->device);
-  if (!g.ok) return fail(CE_ECUDA, "ce_estimate_host: cannot select the handle's device");
+  if (!g.ok) return fail(CE_ECUDA, std::string(who) + ": cannot select the handle's device");
 
-  // Device staging: [y | h | x | soi], each 256-byte aligned, grown on demand.
-  auto al = [](size_t n) { return (n + 255) & ~size_t(255); };
-  const size_t need = al(ny) * 2 + al(nx) + al(size_t(T) * sizeof(int32_t));
-  if (need > h->stage_bytes) {
-    cudaFree(h->d_stage);
-    h->d_stage = nullptr;
-    h->stage_bytes = 0;
-    CE_CUDA(cudaMalloc(&h->d_stage, need), "ce_estimate_host: staging allocation");
-    h->stage_bytes = need;
-  }
   if (h->streams[0] == nullptr) {
     for (auto &s : h->streams) CE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
     CE_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_done) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_in) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     for (auto &e : h->ev_out) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    for (auto &e : h->ev_slot_free) CE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
   }
-  char *base = static_cast<char *>(h->d_stage);
+  // Device staging slot: [y | h | x | soi], each 256-byte aligned, grown on demand (after every call in flight on
+  // the handle's streams has completed: the old buffer may still be read)
+  const int slot = h->next_slot;
+  h->next_slot ^= 1;
+  auto al = [](size_t n) { return (n + 255) & ~size_t(255); };
+  const size_t need = al(ny) * 2 + al(nx) + al(size_t(T) * sizeof(int32_t));
+  if (need > h->stage_bytes[slot]) {
+    for (auto s : h->streams) CE_CUDA(cudaStreamSynchronize(s), "ce_estimate_host: drain before staging growth");
+    cudaFree(h->d_stage[slot]);
+    h->d_stage[slot] = nullptr;
+    h->stage_bytes[slot] = 0;
+    CE_CUDA(cudaMalloc(&h->d_stage[slot], need), "ce_estimate_host: staging allocation");
+    h->stage_bytes[slot] = need;
+  }
+  char *base = static_cast<char *>(h->d_stage[slot]);
   float2 *dy = reinterpret_cast<float2 *>(base);
   float2 *dh = reinterpret_cast<float2 *>(base + al(ny));
   float2 *dx = reinterpret_cast<float2 *>(base + 2 * al(ny));
   int32_t *dsoi = reinterpret_cast<int32_t *>(base + 2 * al(ny) + al(nx));
   cudaStream_t user = static_cast<cudaStream_t>(stream);
   cudaStream_t s_in = h->streams[0], s_k = h->streams[1], s_out = h->streams[2];
-  // order after prior work on the user's stream
+  // order after prior work on the user's stream, and after the previous call on this staging slot
   CE_CUDA(cudaEventRecord(h->ev_start, user), "event record");
   for (auto s : h->streams) CE_CUDA(cudaStreamWaitEvent(s, h->ev_start, 0), "stream wait");
+  CE_CUDA(cudaStreamWaitEvent(s_in, h->ev_slot_free[slot], 0), "stream wait");
   CE_CUDA(cudaMemcpyAsync(dx, x_host, nx, cudaMemcpyHostToDevice, s_in), "x copy");
   if (set_of_instance)
     CE_CUDA(cudaMemcpyAsync(dsoi, set_of_instance, size_t(T) * sizeof(int32_t), cudaMemcpyHostToDevice, s_in),
@@ -503,9 +517,33 @@ int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void 
               "h copy");
     }
   }
+  CE_CUDA(cudaEventRecord(h->ev_slot_free[slot], s_out), "event record");   // the slot's last reader
+  if (sync) {
+    for (int i = 0; i < 3; ++i) CE_CUDA(cudaEventRecord(h->ev_done[i], h->streams[i]), "event record");
+    for (int i = 0; i < 3; ++i) CE_CUDA(cudaStreamWaitEvent(user, h->ev_done[i], 0), "stream wait");
+    CE_CUDA(cudaStreamSynchronize(user), "ce_estimate_host: synchronize");
+  }
+  return CE_OK;
+}
+
+int ce_estimate_host(ce_handle *h, const void *y_host, const void *x_host, void *h_host, int32_t T, int32_t M,
+                     int32_t K, const int32_t *set_of_instance, void *stream) {
+  return estimate_host_impl(h, y_host, x_host, h_host, T, M, K, set_of_instance, stream, true);
+}
+
+int ce_estimate_host_async(ce_handle *h, const void *y_host, const void *x_host, void *h_host, int32_t T, int32_t M,
+                           int32_t K, const int32_t *set_of_instance, void *stream) {
+  return estimate_host_impl(h, y_host, x_host, h_host, T, M, K, set_of_instance, stream, false);
+}
+
+int ce_estimate_host_wait(ce_handle *h, void *stream) {
+  if (h == nullptr) return fail(CE_EINVAL, "ce_estimate_host_wait: NULL handle");
+  if (h->streams[0] == nullptr) return CE_OK;              // no host-path call yet
+  DeviceGuard g(h->device);
+  if (!g.ok) return fail(CE_ECUDA, "ce_estimate_host_wait: cannot select the handle's device");
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < 3; ++i) CE_CUDA(cudaEventRecord(h->ev_done[i], h->streams[i]), "event record");
   for (int i = 0; i < 3; ++i) CE_CUDA(cudaStreamWaitEvent(user, h->ev_done[i], 0), "stream wait");
-  CE_CUDA(cudaStreamSynchronize(user), "ce_estimate_host: synchronize");
   return CE_OK;
 }
 

@@ -229,8 +229,28 @@ __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ 
     const int q0 = MODE == 0 ? 0 : e % GG, q1 = MODE == 0 ? n_out : q0 + 1;
     for (int q = q0; q < q1; ++q) {
       const float2 *w = Ws + ((gq - a) * n_out + q) * GG;
-      // packed FP32x2 complex MACs: (re, im) += l.x (w.re, w.im) + l.y (-w.im, w.re), two FFMA2 per MAC with the
-      // l components as broadcast scalar operands (half the issue slots of four FFMA)
+      // packed FP32x2 complex MACs with the l components as FFMA2's broadcast scalar operand and the weight as
+      // loaded (one 8-byte (re, im) pair): P += l.re w, Q += l.im w, then w l = (P.re - Q.im, P.im + Q.re) --
+      // no (-im, re) weight copy per tap (-DK6_NO_PQ: the earlier (re, im) / (-im, re) pair form)
+#ifndef K6_NO_PQ
+      uint64_t P[RB], Q[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) P[r] = Q[r] = 0ull;
+#pragma unroll
+      for (int j = 0; j < GG; ++j) {
+        const uint64_t wab = *reinterpret_cast<const uint64_t *>(w + j);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          P[r] = fma2(pk2(l[r][j].x, l[r][j].x), wab, P[r]);
+          Q[r] = fma2(pk2(l[r][j].y, l[r][j].y), wab, Q[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const float2 pv = upk2(P[r]), qv = upk2(Q[r]);
+        outs[r * per_row + (MODE == 0 ? q * (K + 1) + gq : e)] = make_float2(pv.x - qv.y, pv.y + qv.x);
+      }
+#else
       uint64_t acc[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = 0ull;
@@ -245,6 +265,7 @@ __global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ 
 #pragma unroll
       for (int r = 0; r < RB; ++r)
         outs[r * per_row + (MODE == 0 ? q * (K + 1) + gq : e)] = upk2(acc[r]);
+#endif
     }
   }
   __syncthreads();

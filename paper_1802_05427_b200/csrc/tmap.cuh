@@ -81,24 +81,26 @@ bool make_map_sw128(CUtensorMap *m, const void *ptr, int N, long long rows, int 
 // back-to-back calls on the same buffers skip the driver encode.
 struct MapCacheEntry {
   const void *ptr;
-  int N, box_rows;
+  int N, box_rows, box_floats;
   long long rows;
   bool sw128;
   CUtensorMap map;
 };
-bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows, bool sw128 = false) {
-  constexpr int NC = 24;
+bool cached_map(CUtensorMap *m, const void *ptr, int N, long long rows, int box_rows, bool sw128 = false,
+                int box_floats = 32) {
+  constexpr int NC = 32;
   static thread_local MapCacheEntry cache[NC];
   static thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i)
     if (cache[i].ptr == ptr && cache[i].N == N && cache[i].rows == rows && cache[i].box_rows == box_rows &&
-        cache[i].sw128 == sw128) {
+        cache[i].sw128 == sw128 && cache[i].box_floats == box_floats) {
       *m = cache[i].map;
       return true;
     }
-  if (!(sw128 ? make_map_sw128(m, ptr, N, rows, box_rows) : make_map(m, ptr, N, rows, box_rows))) return false;
+  if (!(sw128 ? make_map_sw128(m, ptr, N, rows, box_rows) : make_map(m, ptr, N, rows, box_rows, box_floats)))
+    return false;
   MapCacheEntry &e = cache[next];
-  e = MapCacheEntry{ptr, N, box_rows, rows, sw128, *m};
+  e = MapCacheEntry{ptr, N, box_rows, box_floats, rows, sw128, *m};
   next = (next + 1) % NC;
   if (used < NC) ++used;
   return true;
