@@ -183,7 +183,7 @@ __device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {  
   return r;
 }
 template <int MODE, int GG, int SS>
-__global__ void __launch_bounds__(128) k6_estimate_g(const float2 *__restrict__ y, const float2 *__restrict__ x,
+__global__ void __launch_bounds__(128, 4) k6_estimate_g(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                      const float2 *__restrict__ W, float2 *__restrict__ h,
                                                      int M, CombGeo g) {
   extern __shared__ float2 sm6[];
