@@ -798,30 +798,55 @@ def run_stats(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     samples = cfg.T * cfg.M * cfg.K * cfg.N
     cols = cfg.T * cfg.M * cfg.K
+    peaks = _peaks()
+    fp32_peak = peaks.get("fp32_tflops", 69.13) * 1e12
+    hbm_bw = peaks.get("hbm_gbs", 6548.8) * 1e9
+    bf16 = peaks.get("bf16_tflops", 1605.7) * 1e12
+    # the library's policy (k7_stats.cu, k9_spectrum.cu): lags through the power spectrum (K9: FP32 FFT of length
+    # L = 2^l >= max(64, N + D - 1) per LS row, l <= 13) and the noise window on the tensor cores (K4 power mode:
+    # one BF16x3 pass over y against the inverse-DFT bank) when K4 can stream y (N even, K <= 32)
+    L = 64
+    while L < cfg.N + D - 1:
+        L *= 2
+    k9 = L <= 8192 and cfg.n_sets <= 65535
+    k4n = k9 and cfg.N % 2 == 0 and cfg.K <= 32 and B <= 4096
+    y_bytes = float(y.nbytes)
+    x_bytes = float(x.nbytes)
+    fft_flops = 5.0 * L * np.log2(L) * cols                # the standard radix-2 count, per zero-padded row
     lag_flops = 8.0 * cols * sum(cfg.N - d for d in range(D))
     noise_flops = 8.0 * cols * cfg.N * B
-    flops = lag_flops + noise_flops
-    props = torch.cuda.get_device_properties(0)
-    fp32_peak = props.multi_processor_count * 128 * 2 * 1965e6
-    # the library's policy (k7_stats.cu): lags on the tensor cores (K8, BF16x3) from 16384 columns, noise window then
-    # streamed by K7c; below, K7a does both on the FP32 pipes
-    k8 = cols >= 16384 and cfg.K <= 24 and D <= 512 and cfg.N % 2 == 0
-    bf16 = _peaks().get("bf16_tflops", 1605.7) * 1e12
-    t_ideal = (lag_flops / (bf16 / 3) + noise_flops / fp32_peak) if k8 else flops / fp32_peak
+    if k9 and k4n:
+        # K9 bound by the FP32 pipes or by its read of y; K4's noise pass bound by its read of y (HBM)
+        t_k9 = max(fft_flops / fp32_peak, (y_bytes + x_bytes) / hbm_bw)
+        t_k4 = (y_bytes + x_bytes) / hbm_bw
+        t_ideal = t_k9 + t_k4
+        bound, kern = "alu+hbm", "k9_spectrum (lags) + k4_bf16x3 power mode (noise window)"
+        note = ("sum of the two kernels' bounds: K9 = max(FFT flops 5 L log2 L per row at the FP32 FFMA peak, y + x "
+                "bytes at HBM), K4 noise pass = y + x bytes at HBM")
+        flops = fft_flops + 3 * 8.0 * cols * cfg.N * B
+    else:
+        t_ideal = lag_flops / (bf16 / 3) + noise_flops / fp32_peak
+        bound, kern = "tensor+alu", "k8_gram / k7_accumulate (lags) + k7_noise (noise window)"
+        note = "lag flops at the BF16 peak / 3 plus noise-window flops at the FP32 SIMT peak"
+        flops = lag_flops + noise_flops
+    t_direct = lag_flops / (bf16 / 3) + noise_flops / fp32_peak
     line = {"metric": "LS samples/s through the statistics estimator (NEXT-3)", "value": samples / (ms * 1e-3),
             "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c64 I/O; lags bf16x3 tensor products (K8) or fp32 FFMA; fp64 accumulation per set",
+            "dtype": ("c64 I/O; lags fp32 FFT, noise window bf16x3 tensor products; fp64 accumulation per set"
+                      if k9 and k4n else "c64 I/O; lags bf16x3 tensor products (K8) or fp32 FFMA; fp64 accumulation per set"),
             "data": "synthetic (seeded workload generator)",
-            "config": _cfg_json(cfg, {"D": D, "B": B, "l2": f"rotating {nbuf} y buffers (> L2)"}),
-            "roofline": {"bound": "tensor+alu" if k8 else "alu", "achieved": flops / (ms * 1e-3) / 1e12,
-                         "peak": flops / t_ideal / 1e12, "unit": "TFLOP/s", "frac": t_ideal / (ms * 1e-3),
-                         "traffic": None, "roofline_time_us": t_ideal * 1e6,
-                         "kernel": "k8_gram (lags) + k7_noise (noise window)" if k8 else "k7_accumulate",
-                         "algorithmic_flops_per_launch": flops,
-                         "note": ("effective peak of the mix: lag flops at the BF16 peak / 3 (BF16x3) plus noise-window "
-                                  "flops at the FP32 SIMT peak" if k8 else "lag + noise-window flops vs the FP32 SIMT peak")},
-            "gpu_launches": (3 if k8 else 2) * args.steps, "clocks": clk.summary(), "device": props.name}
+            "config": _cfg_json(cfg, {"D": D, "B": B, "L_fft": L if k9 else None,
+                                      "l2": f"rotating {nbuf} y buffers (> L2)"}),
+            "roofline": {"bound": bound, "achieved": None, "peak": None, "unit": "us", "frac": t_ideal / (ms * 1e-3),
+                         "traffic": None, "roofline_time_us": t_ideal * 1e6, "kernel": kern,
+                         "flops_per_launch": flops, "note": note,
+                         "direct_method_roofline_us": t_direct * 1e6,
+                         "frac_vs_direct_method": t_direct / (ms * 1e-3),
+                         "direct_method_note": ("round-1/2a definition: the direct lag sums 8 C sum_d (N - d) at the "
+                                                "BF16 peak / 3 plus the noise-window DFT 8 C N B at the FP32 peak")},
+            "gpu_launches": (5 if k9 and k4n else 3) * args.steps, "clocks": clk.summary(),
+            "device": torch.cuda.get_device_properties(0).name}
     print(json.dumps(line), flush=True)
 
 

@@ -219,14 +219,19 @@ int ce_comb_free(ce_comb_handle *h);
  * The results can be handed (via the host) to ce_init as r_hh (entries d >= D may be zero when D >= b:
  * the filters use d < b only) and sigma2.
  * ------------------------------------------------------------------------------------------------- */
-/* Bytes of device workspace ce_stats_estimate needs: n_sets * (2 D + 2) doubles. */
-int ce_stats_workspace_bytes(int32_t n_sets, int32_t D, int64_t *out);
-/* Device pointers, asynchronous on `stream` (K7a accumulate + K7b normalise; from 16384 columns T*M*K up, with
- * K <= 24, D <= 512, N even and d_y 16-byte aligned, the lag sums run on the tensor cores as a banded Gram
- * matrix (K8, BF16x3) and the noise floor is streamed by K7c -- same results within the 1e-4 parity bar):
+/* Bytes of device workspace ce_stats_estimate needs for (N, n_sets, D, B): the per-set accumulators
+ * (n_sets * (2 D + 2) doubles, rounded up to 256 bytes) plus, when L = the smallest power of two >= max(64, N + D - 1)
+ * is at most 8192, the per-set power spectra (n_sets * L doubles).  CE_EINVAL for N < 2, n_sets, D or B < 1, NULL out. */
+int ce_stats_workspace_bytes(int32_t N, int32_t n_sets, int32_t D, int32_t B, int64_t *out);
+/* Device pointers, asynchronous on `stream`.  The lag sums: when L (above) is at most 8192 and n_sets <= 65535,
+ * through the power spectrum of the zero-padded LS rows (K9: FP32 FFT of length L per row, |X|^2 summed per set in
+ * FP64, then the FP64 inverse DFT at d < D -- the Wiener-Khinchin identity, no wrap for L >= N + D - 1); else from
+ * 16384 columns T*M*K up, with K <= 24, D <= 512, N even and d_y 16-byte aligned, on the tensor cores as a banded
+ * Gram matrix (K8, BF16x3); else as direct sums (K7a).  The noise floor: streamed by K7c (N even, d_y 16-byte
+ * aligned) when the lags ran elsewhere, else inside K7a; K7b normalises.  Every path meets the same 1e-4 parity bar:
  *   d_y [T][M][K][N], d_x [T][K][N] complex64 (8-byte aligned); d_set_of_instance int32 [T] or NULL (all
  *   set 0; instances with an out-of-range set are skipped); d_r out: complex128 [n_sets][D] interleaved;
- *   d_sigma2 out: float64 [n_sets]; d_work: ce_stats_workspace_bytes bytes.  A set with no instance gets
+ *   d_sigma2 out: float64 [n_sets]; d_work: ce_stats_workspace_bytes(N, n_sets, D, B) bytes, 8-byte aligned.  A set with no instance gets
  *   NaN.  CE_EINVAL for NULL / misaligned pointers, sizes < 1, D or B > N, N > 12800. */
 int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, int32_t K, int32_t N,
                       const int32_t *d_set_of_instance, int32_t n_sets, int32_t D, int32_t B, void *d_r,

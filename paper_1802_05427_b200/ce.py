@@ -53,7 +53,7 @@ lib.ce_comb_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32
 lib.ce_comb_get_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_comb_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
 lib.ce_comb_free.argtypes = [c_void_p]
-lib.ce_stats_workspace_bytes.argtypes = [c_int32, c_int32, POINTER(c_int64)]
+lib.ce_stats_workspace_bytes.argtypes = [c_int32, c_int32, c_int32, c_int32, POINTER(c_int64)]
 lib.ce_stats_estimate.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int32,
                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
 lib.ce_build_filters.argtypes = [c_void_p, c_void_p]
@@ -388,7 +388,7 @@ def ce_stats_estimate(y, x, D: int, B: int, set_of_instance=None, n_sets: int = 
             raise TypeError("set_of_instance must be a CUDA int32 tensor")
         soi = set_of_instance.data_ptr()
     nb = c_int64()
-    _check(lib.ce_stats_workspace_bytes(n_sets, D, ctypes.byref(nb)), "ce_stats_workspace_bytes")
+    _check(lib.ce_stats_workspace_bytes(N, n_sets, D, B, ctypes.byref(nb)), "ce_stats_workspace_bytes")
     work = torch.empty(nb.value // 8, dtype=torch.float64, device=y.device)
     r = torch.empty((n_sets, D), dtype=torch.complex128, device=y.device)
     s2 = torch.empty((n_sets,), dtype=torch.float64, device=y.device)

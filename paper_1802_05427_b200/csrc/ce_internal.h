@@ -34,6 +34,14 @@ struct ContractArgs {
   const int32_t *soi;      // [T] device or nullptr
   int32_t T, M, K, N, b, n_win, n_sets, max_kept;
   bool even_starts;        // every window start a_w is even (16-byte aligned TMA boxes, K4)
+  // K4 power mode (the statistics estimator's noise window, k7_stats.cu): no h stores; each tile adds the sum of
+  // |output|^2 over its rows to pow_acc[set * pow_stride] and, for window 0, its row count to
+  // pow_acc[set * pow_stride + 1].  bank_rows (> 0) overrides the bank's rows per K chunk; bank_shared: one bank for
+  // every set.
+  double *pow_acc = nullptr;
+  int32_t pow_stride = 0;
+  int32_t bank_rows = 0;
+  bool bank_shared = false;
 };
 
 // K1: filter build.  Returns cudaError_t of the launches.
@@ -60,12 +68,24 @@ cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets,
                                    uint16_t *bank_lo, cudaStream_t stream, int64_t *launches);
 cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches);
+// K4's bank for the unitary N-point inverse DFT at the B delay bins lo .. lo + B - 1 (rows = bins, K = tones): one
+// set, nkc = ceil(2N / 32) chunks of NR = ceil(2B / 16) * 16 rows, bf16 hi / lo planes.
+void dft_bank_shape(int32_t N, int32_t B, int32_t *nkc, int32_t *NR);
+cudaError_t launch_build_dft_bank(int32_t N, int32_t B, int32_t lo, uint16_t *bank_hi, uint16_t *bank_lo,
+                                  cudaStream_t stream);
 
 
 // K8: the statistics estimator's lag correlation (banded Gram matrix) on tcgen05; adds into K7's accumulator.
 bool gram_launchable(const float2 *y, int32_t K, int32_t N, int32_t D);
 cudaError_t launch_gram(const float2 *y, const float2 *x, int32_t T, int32_t M, int32_t K, int32_t N,
                         const int32_t *soi, int32_t n_sets, int32_t D, double *acc, cudaStream_t stream);
+
+// K9: the lag correlation through the power spectrum of the zero-padded LS rows (FFT of length L = 2^l >= N + D - 1);
+// spectrum_log2 returns l, or -1 when L would exceed 8192.  P: [n_sets][L] FP64 workspace; writes acc[s][0 .. 2D).
+int spectrum_log2(int32_t N, int32_t D);
+cudaError_t launch_spectrum_lags(const float2 *y, const float2 *x, int32_t T, int32_t M, int32_t K, int32_t N,
+                                 const int32_t *soi, int32_t n_sets, int32_t D, double *P, double *acc,
+                                 cudaStream_t stream);
 
 void set_last_error(const std::string &msg);
 

@@ -99,6 +99,9 @@ struct K4Params {
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
   int l2_hint;               // bit 0: y loads evict_first; 1: h TMA stores evict_first; 2: x loads evict_last;
                              // 3: filter-bank loads evict_last (experiments beyond bit 0)
+  double *pow_acc;           // power mode (ContractArgs::pow_acc): per-set sum of |out|^2 and row count, no stores
+  int pow_stride;
+  int bank_shared;           // 1: one bank for every set
   Window geo_s[MAXW_PARAM];
 };
 
@@ -222,6 +225,46 @@ __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *
   }
 }
 
+// Power mode: the sum of |output|^2 over this warp's 32 rows of a finished tile (kept range only, rows inside the
+// instance) and, for window 0, the row count, added to the set's FP64 accumulators.
+__device__ __forceinline__ void epi_power(const K4Params &p, uint32_t tmem_base, const Tile4 &ti, int ncb, int q,
+                                          int lane, int acc, bool set_ok) {
+  const int rA = lane >> 2, cq = lane & 3;
+  const int nf = 2 * ti.kept;
+  const int c0 = ti.ct * TM + q * 32 + rA;           // rows c0, c0 + 8, c0 + 16, c0 + 24
+  const bool r0 = c0 < p.cols, r1 = c0 + 8 < p.cols, r2 = c0 + 16 < p.cols, r3 = c0 + 24 < p.cols;
+  float pw = 0.f;
+  for (int cb = 0; cb < ncb; ++cb) {
+    uint32_t v0[16], v1[16];
+    const uint32_t ta = tmem_base + uint32_t(acc * NMAXW + cb * 32) + (uint32_t(q * 32) << 16);
+    tmem_ld16x256b_x4(ta, v0);
+    tmem_ld16x256b_x4(ta + (16u << 16), v1);
+    tmem_ld_wait();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int f = cb * 32 + 8 * m + 2 * cq - ti.off;
+      if (f >= 0 && f < nf) {
+        const float a0 = __uint_as_float(v0[4 * m]), a1 = __uint_as_float(v0[4 * m + 1]);
+        const float b0 = __uint_as_float(v0[4 * m + 2]), b1 = __uint_as_float(v0[4 * m + 3]);
+        const float c0_ = __uint_as_float(v1[4 * m]), c1 = __uint_as_float(v1[4 * m + 1]);
+        const float d0 = __uint_as_float(v1[4 * m + 2]), d1 = __uint_as_float(v1[4 * m + 3]);
+        if (r0) pw = fmaf(a0, a0, fmaf(a1, a1, pw));
+        if (r1) pw = fmaf(b0, b0, fmaf(b1, b1, pw));
+        if (r2) pw = fmaf(c0_, c0_, fmaf(c1, c1, pw));
+        if (r3) pw = fmaf(d0, d0, fmaf(d1, d1, pw));
+      }
+    }
+  }
+  double s = pw;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0 && set_ok) {
+    double *a = p.pow_acc + size_t(tile_set(p, ti.t)) * p.pow_stride;
+    atomicAdd(a, s);
+    if (ti.o == 0) atomicAdd(a + 1, double(min(32, max(0, p.cols - (ti.ct * TM + q * 32)))));
+  }
+}
+
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
               const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K4Params p) {
@@ -302,7 +345,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   // filter bank, which ce_build_filters completed (stream-synchronised) before any estimate could be
   // enqueued, so its first chunks are fetched while the previous kernel drains.
 #ifndef K4_NO_PDL
-  if (!(warp == 14 && p.soi == nullptr)) pdl_wait();
+  if (!(warp == 14 && p.soi == nullptr && p.pow_acc == nullptr)) pdl_wait();   // power mode: bank built just before
 #endif
 #ifdef CE_K4_TRACE
   unsigned long long c_pdl = clock64(), c_dec = 0, c_tma0 = 0, c_w0 = 0;   // producer prologue, stored at the end
@@ -433,7 +476,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       tc_fence_after();
       if (tid == 256 && lt < 8) K4TR(136 + lt);
       const int ncb = (ti.off + 2 * ti.kept + 31) / 32;
-      for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok);
+      if (p.pow_acc) {
+        epi_power(p, tmem_base, ti, ncb, q, lane, acc, set_ok);
+      } else {
+        for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok);
+      }
       if (tid == 256 && lt < 8) K4TR(144 + lt);
       __syncwarp();
       if (lane == 0) {
@@ -448,7 +495,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       int it = 0;
       for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
         const Tile4 ti = decode4(p, g);
-        const int set = max(tile_set(p, ti.t), 0);
+        const int set = p.bank_shared ? 0 : max(tile_set(p, ti.t), 0);
         const uint32_t bytes = uint32_t(ti.nw) * 64;          // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
@@ -559,6 +606,36 @@ __global__ void k4_build_bank(const float2 *__restrict__ W, int b, int nkc, int 
   }
 }
 
+// bank[kc][n][32] of the unitary inverse DFT rows W[i][j] = e^{+2 pi i j (lo + i) / N} / sqrt(N), i < B, j < N
+// (zero beyond), same embedding and SW64 image as k4_build_bank; the angle reduced exactly in integers, FP64 sincospi.
+__global__ void k4_build_dft_bank(int N, int B, int lo, int nkc, int NR, uint16_t *__restrict__ bank_hi,
+                                  uint16_t *__restrict__ bank_lo) {
+  const int kc = blockIdx.x;
+  uint16_t *bh = bank_hi + size_t(kc) * NR * 32;
+  uint16_t *bl = bank_lo + size_t(kc) * NR * 32;
+  const double inv_sqrt_n = 1.0 / sqrt(double(N));
+  for (int e = threadIdx.x; e < NR * 32; e += blockDim.x) {
+    const int n = e / 32, kk = e % 32;
+    const int k = kc * 32 + kk;
+    const int i = n >> 1, jw = k >> 1;
+    float v = 0.f;
+    if (i < B && jw < N) {
+      const long long m = (static_cast<long long>(jw) * (lo + i)) % N;
+      double sv, cv;
+      sincospi(2.0 * double(m) / double(N), &sv, &cv);
+      const float2 w = make_float2(float(cv * inv_sqrt_n), float(sv * inv_sqrt_n));
+      const int sel = ((n & 1) << 1) | (k & 1);
+      v = sel == 0 ? w.x : sel == 1 ? -w.y : sel == 2 ? w.y : w.x;
+    }
+    const uint32_t hi2 = pack_bf16(v, 0.f);
+    const float hi = bf16_lo_f(hi2);
+    const uint32_t lo2 = pack_bf16(v - hi, 0.f);
+    const int dst = n * 32 + ((((kk >> 3) ^ ((n >> 1) & 3))) << 3) + (kk & 7);
+    bh[dst] = uint16_t(hi2 & 0xFFFFu);
+    bl[dst] = uint16_t(lo2 & 0xFFFFu);
+  }
+}
+
 // Per-device launch facts: smem attribute set once, SM count.
 struct DevInfo {
   bool init = false;
@@ -593,6 +670,19 @@ extern "C" int ce_k4_trace_set(void *dptr) {
 void bf16x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR) {
   *nkc = (2 * b + 31) / 32;
   *NR = ((2 * b + 16) + 7) & ~7;
+}
+
+void dft_bank_shape(int32_t N, int32_t B, int32_t *nkc, int32_t *NR) {
+  *nkc = (2 * N + 31) / 32;
+  *NR = (2 * B + 15) & ~15;
+}
+
+cudaError_t launch_build_dft_bank(int32_t N, int32_t B, int32_t lo, uint16_t *bank_hi, uint16_t *bank_lo,
+                                  cudaStream_t stream) {
+  int32_t nkc, NR;
+  dft_bank_shape(N, B, &nkc, &NR);
+  k4_build_dft_bank<<<nkc, 256, 0, stream>>>(N, B, lo, nkc, NR, bank_hi, bank_lo);
+  return cudaGetLastError();
 }
 
 bool bf16x3_launchable(const ContractArgs &a) {
@@ -632,6 +722,10 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   p.n_win = a.n_win;
   p.n_sets = a.n_sets;
   bf16x3_bank_shape(a.b, &p.nkc, &p.NR);
+  if (a.bank_rows > 0) p.NR = a.bank_rows;
+  p.pow_acc = a.pow_acc;
+  p.pow_stride = a.pow_stride;
+  p.bank_shared = a.bank_shared ? 1 : 0;
   p.cols = a.M * a.K;
   p.n_ct = (p.cols + TM - 1) / TM;
   for (int w = 0; w < MAXW_PARAM; ++w) p.geo_s[w] = w < a.n_win && a.geo_host ? a.geo_host[w] : Window{0, 0, 0};
@@ -645,7 +739,7 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   // TMA stores pay off when CTAs walk several tiles (their stores overlap the next tiles' loads; measured
   // -11% on config 5); a one-tile-per-SM launch (config 3) keeps the 4-deep raw ring and direct stores.
   static const int env_st = getenv("CE_K4_TMA_STORE") ? atoi(getenv("CE_K4_TMA_STORE")) : -1;   // experiments
-  const bool st_ok = (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0;
+  const bool st_ok = (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0 && a.pow_acc == nullptr;
   p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) && st_ok;
   static const int env_last = getenv("CE_K4_TMA_LAST") ? atoi(getenv("CE_K4_TMA_LAST")) : 1;   // experiments
   p.tma_last = env_last != 0 && st_ok && S_AB * AB_STAGE >= 4 * 8 * EPI_WARP;

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "ce_internal.h"
 #include "tc_ptx.cuh"
@@ -453,14 +454,33 @@ __global__ void k7_finalize(const double *__restrict__ acc, int n_sets, int N, i
 }  // namespace
 }  // namespace ce
 
+namespace {
+// workspace layout: the per-set accumulators (K7's layout) then, 256-byte aligned, K9's per-set spectra
+size_t stats_acc_bytes(int32_t n_sets, int32_t D) {
+  return ((size_t(n_sets) * (2 * size_t(D) + 2) * sizeof(double)) + 255) & ~size_t(255);
+}
+size_t stats_spectrum_bytes(int32_t N, int32_t n_sets, int32_t D) {
+  const int l = ce::spectrum_log2(N, D);
+  return ((l < 0 ? 0 : size_t(n_sets) * (size_t(1) << l) * sizeof(double)) + 255) & ~size_t(255);
+}
+// K4's inverse-DFT bank for the noise window: hi and lo bf16 planes
+size_t stats_bank_plane_bytes(int32_t N, int32_t B) {
+  int32_t nkc, NR;
+  ce::dft_bank_shape(N, B, &nkc, &NR);
+  return ((size_t(nkc) * NR * 32 * sizeof(uint16_t)) + 255) & ~size_t(255);
+}
+constexpr int32_t K4_NOISE_MAX_B = 32 * 128;   // windows of 128 bins carried in K4's kernel parameters
+}  // namespace
+
 extern "C" {
 
-int ce_stats_workspace_bytes(int32_t n_sets, int32_t D, int64_t *out) {
-  if (out == nullptr || n_sets < 1 || D < 1) {
-    ce::set_last_error("ce_stats_workspace_bytes: need n_sets >= 1, D >= 1, out != NULL");
+int ce_stats_workspace_bytes(int32_t N, int32_t n_sets, int32_t D, int32_t B, int64_t *out) {
+  if (out == nullptr || N < 2 || n_sets < 1 || D < 1 || B < 1) {
+    ce::set_last_error("ce_stats_workspace_bytes: need N >= 2, n_sets >= 1, D >= 1, B >= 1, out != NULL");
     return CE_EINVAL;
   }
-  *out = int64_t(n_sets) * (2 * int64_t(D) + 2) * int64_t(sizeof(double));
+  *out = int64_t(stats_acc_bytes(n_sets, D) + stats_spectrum_bytes(N, n_sets, D) +
+                 (B <= K4_NOISE_MAX_B ? 2 * stats_bank_plane_bytes(N, B) : 0));
   return CE_OK;
 }
 
@@ -487,7 +507,9 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
   // K8 pays a per-unit factor table and diagonal-bin epilogue: measured faster from config 4's 61440 columns
   // up (config 4: 2.4 vs 4.1 ms, config 5: 9.7 vs 17.2 ms) and slower on config 3's 1536 (164 vs 147 us)
   const bool k8 = gram && (cols >= 16384 || env_gram == 1) && ce::gram_launchable(static_cast<const float2 *>(d_y), K, N, D);
-  int cpb = k8 ? 8 : ce::K7_CPB;
+  static const int env_k9 = getenv("CE_K9") ? atoi(getenv("CE_K9")) : -1;   // experiments: 0 off
+  const bool k9 = env_k9 != 0 && ce::spectrum_log2(N, D) >= 0 && n_sets <= 65535;
+  int cpb = (k8 || k9) ? 8 : ce::K7_CPB;
   if (env_cpb > 0) cpb = env_cpb;
   cpb = std::max(1, std::min(cpb, M * K));
   const long long ctas = (long long)T * ((static_cast<long long>(M) * K + cpb - 1) / cpb);
@@ -507,9 +529,20 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     ce::set_last_error(std::string("ce_stats_estimate: ") + cudaGetErrorString(e));
     return CE_ECUDA;
   }
-  // the lag correlation on the tensor cores (K8) when it fits; K7 then adds the noise floor and column count
+  // the lag correlation: through the power spectrum (K9, FFT of the zero-padded LS rows) when L = 2^l >= N + D - 1
+  // fits 8192, else on the tensor cores (K8) from 16384 columns, else inside K7a's pass (direct sums); K7 then adds
+  // the noise floor and the column count
   int k7_lags = D;
-  if (k8) {
+  if (k9) {
+    double *P = reinterpret_cast<double *>(static_cast<char *>(d_work) + stats_acc_bytes(n_sets, D));
+    e = ce::launch_spectrum_lags(static_cast<const float2 *>(d_y), static_cast<const float2 *>(d_x), T, M, K, N,
+                                 d_set_of_instance, n_sets, D, P, acc, st);
+    if (e != cudaSuccess) {
+      ce::set_last_error(std::string("ce_stats_estimate: K9 launch: ") + cudaGetErrorString(e));
+      return CE_ECUDA;
+    }
+    k7_lags = 0;
+  } else if (k8) {
     e = ce::launch_gram(static_cast<const float2 *>(d_y), static_cast<const float2 *>(d_x), T, M, K, N,
                         d_set_of_instance, n_sets, D, acc, st);
     if (e != cudaSuccess) {
@@ -518,14 +551,54 @@ int ce_stats_estimate(const void *d_y, const void *d_x, int32_t T, int32_t M, in
     }
     k7_lags = 0;
   }
-  // the noise window streamed by K7c (N even, y 16-byte aligned; bins in passes of 32) when K8 has the
-  // lags, else inside K7a's pass over the LS rows (measured: K7a alone 116 us vs K7a lags + K7c 133 us on config 3;
-  // with K8, config 4 2.15 -> 1.60 ms, config 5 11.9 -> 6.1 ms)
+  // the noise window when the lags ran elsewhere: on the tensor cores by K4 in power mode (the unitary inverse DFT at
+  // the B bins as a BF16x3 bank, LS division fused, sum of |.|^2 per set; needs K4's TMA conditions), else streamed
+  // by K7c (N even, y 16-byte aligned; bins in passes of 32), else inside K7a's pass (measured: K7a alone 116 us vs
+  // K7a lags + K7c 133 us on config 3; with K8, config 4 2.15 -> 1.60 ms, config 5 11.9 -> 6.1 ms)
   static const int env_nz = getenv("CE_K7_NOISE") ? atoi(getenv("CE_K7_NOISE")) : -1;   // experiments: 0 off, 1 force
   static const int env_mpb = getenv("CE_K7_MPB") ? atoi(getenv("CE_K7_MPB")) : 0;
-  const bool k7c = (env_nz == 1 || (env_nz != 0 && k7_lags == 0)) && N % 2 == 0 &&
+  static const int env_k4n = getenv("CE_K4_NOISE") ? atoi(getenv("CE_K4_NOISE")) : -1;   // experiments: 0 off
+  std::vector<ce::Window> nwin;
+  for (int32_t o = 0; o < B; o += 128) nwin.push_back(ce::Window{0, o, std::min(B, o + 128)});
+  ce::ContractArgs na;
+  na.y = static_cast<const float2 *>(d_y);
+  na.x = static_cast<const float2 *>(d_x);
+  na.h = nullptr;
+  na.Wt = nullptr;
+  na.geo = nullptr;
+  na.geo_host = nwin.data();
+  na.soi = d_set_of_instance;
+  na.T = T;
+  na.M = M;
+  na.K = K;
+  na.N = N;
+  na.b = N;
+  na.n_win = int32_t(nwin.size());
+  na.n_sets = n_sets;
+  na.max_kept = std::min(B, 128);
+  na.even_starts = true;
+  na.pow_acc = acc + 2 * D;
+  na.pow_stride = 2 * D + 2;
+  int32_t bank_nkc = 0, bank_NR = 0;
+  ce::dft_bank_shape(N, B, &bank_nkc, &bank_NR);
+  na.bank_rows = bank_NR;
+  na.bank_shared = true;
+  const bool k4n = env_k4n != 0 && env_nz != 1 && k7_lags == 0 && B <= K4_NOISE_MAX_B && ce::bf16x3_launchable(na);
+  if (k4n) {
+    char *wb = static_cast<char *>(d_work) + stats_acc_bytes(n_sets, D) + stats_spectrum_bytes(N, n_sets, D);
+    uint16_t *bank_hi = reinterpret_cast<uint16_t *>(wb);
+    uint16_t *bank_lo = reinterpret_cast<uint16_t *>(wb + stats_bank_plane_bytes(N, B));
+    e = ce::launch_build_dft_bank(N, B, N / 2 - B / 2, bank_hi, bank_lo, st);
+    int64_t nl = 0;
+    if (e == cudaSuccess) e = ce::launch_contract_bf16x3(na, bank_hi, bank_lo, st, &nl);
+    if (e != cudaSuccess) {
+      ce::set_last_error(std::string("ce_stats_estimate: K4 noise-window launch: ") + cudaGetErrorString(e));
+      return CE_ECUDA;
+    }
+  }
+  const bool k7c = !k4n && (env_nz == 1 || (env_nz != 0 && k7_lags == 0)) && N % 2 == 0 &&
                    (reinterpret_cast<uintptr_t>(d_y) & 15u) == 0;
-  if (k7_lags > 0 || !k7c) {
+  if (!k4n && (k7_lags > 0 || !k7c)) {   // K7a: the lags (unless K9 / K8 ran) and the noise window (unless K7c runs)
     ce::k7_accumulate<<<unsigned(ctas), ce::K7_THREADS, smem, st>>>(static_cast<const float2 *>(d_y),
                                                                     static_cast<const float2 *>(d_x), M, K, N,
                                                                     d_set_of_instance, n_sets, D, B, acc, k7_lags, cpb,

@@ -100,6 +100,26 @@ def test_stats_skipped_and_empty_sets():
     assert np.isnan(s2_g[1]) and np.isnan(r_g[2]).all()                     # sets with no instance
 
 
+@pytest.mark.parametrize("N,D,B", [(40, 25, 8), (100, 20, 16), (200, 50, 24), (400, 100, 32), (700, 200, 32),
+                                   (1200, 150, 32), (3276, 126, 32), (5000, 200, 64), (1201, 64, 31)])
+def test_stats_spectrum_lengths(N, D, B):
+    """The power-spectrum lag path (K9) at every FFT length it instantiates: L = 64 .. 8192, i.e. every final-pass
+    radix (16 x 4, 16 x 8, 16 x 16, 16 x 16 x 2, ... 16 x 16 x 16 x 2); an odd N takes the K7a noise window."""
+    rng = np.random.default_rng(N + D)
+    T, M, K = 2, 5, 3
+    x = np.exp(1j * np.pi / 2 * rng.integers(0, 4, (T, K, N)) + 1j * np.pi / 4).astype(np.complex64)
+    # a smooth channel (few delay taps) plus white noise, so that the lags decay as in the workloads
+    taps = rng.standard_normal((T, M, K, 4)) + 1j * rng.standard_normal((T, M, K, 4))
+    n = np.arange(N)
+    Hc = sum(taps[..., i:i + 1] * np.exp(-2j * np.pi * 3 * i * n / N) for i in range(4))
+    noise = 0.1 * (rng.standard_normal((T, M, K, N)) + 1j * rng.standard_normal((T, M, K, N)))
+    y = ((Hc + noise) * x[:, None, :, :]).astype(np.complex64)
+    r_g, s2_g = _gpu_stats(y, x, D, B)
+    r_o, s2_o = oracle.estimate_stats(y, x, D, B)
+    assert abs(s2_g[0] / s2_o - 1) < 1e-4, (s2_g[0], s2_o)
+    assert np.max(np.abs(r_g[0] - r_o)) < 1e-4 * abs(r_o[0]), np.max(np.abs(r_g[0] - r_o)) / abs(r_o[0])
+
+
 def test_estimated_statistics_drive_the_filters():
     """Data-driven design: K7 statistics -> ce_init/ce_build_filters -> K4 estimate.  The MSE vs the true
     channel is close to the matched closed form (the paper's fixed design is not needed)."""
@@ -121,13 +141,18 @@ def test_estimated_statistics_drive_the_filters():
     assert mse < 1.10 * cf, (mse, cf)
 
 
-@pytest.mark.parametrize("env", [{"CE_K8_GRAM": "1"}, {"CE_K8_GRAM": "0", "CE_K7_NOISE": "0"},
-                                 {"CE_K8_GRAM": "0", "CE_K7_NOISE": "1"}], ids=["k8_forced", "k7a_only", "k7a_k7c"])
+@pytest.mark.parametrize("env", [{"CE_K9": "0", "CE_K8_GRAM": "1", "CE_K4_NOISE": "0"},
+                                 {"CE_K9": "0", "CE_K8_GRAM": "0", "CE_K7_NOISE": "0"},
+                                 {"CE_K9": "0", "CE_K8_GRAM": "0", "CE_K7_NOISE": "1"},
+                                 {"CE_K4_NOISE": "0", "CE_K7_NOISE": "0"},
+                                 {"CE_K4_NOISE": "0"}],
+                         ids=["k8_k7c", "k7a_only", "k7a_k7c", "k9_k7a_noise", "k9_k7c"])
 def test_stats_parity_other_kernel_paths(env):
-    """The statistics parity tests again (i) with the tensor-core lag correlation (K8) forced on every shape (by
-    default it runs only from 16384 columns up; K7c then streams the noise window), (ii) with K7a alone (lags and
-    noise window in one pass, K8 and K7c off), (iii) K7a lags + K7c noise window, in a subprocess: the variables
-    are read once per process."""
+    """The statistics parity tests again with the other kernel paths (by default the lags go through the power
+    spectrum, K9, and the noise window through K4 in power mode): (i) the tensor-core lag correlation (K8) forced on
+    every shape with K7c streaming the noise window, (ii) K7a alone (lags and noise window in one pass), (iii) K7a
+    lags + K7c, (iv) K9 lags + the noise window in K7a, (v) K9 + K7c; in a subprocess: the variables are read once
+    per process."""
     import os
     import subprocess
     import sys
