@@ -686,7 +686,8 @@ def run_ours(args, cfg):
 
 
 def run_comb(args):
-    """--comb NAME: the paper's comb-pilot 3W / 12W-LMMSE path (NEXT-1, K6) on one of workload.COMB_CONFIGS."""
+    """--comb NAME: the paper's comb-pilot 3W / 12W-LMMSE path (NEXT-1; K10 on tcgen05 for the 12W, K6b FP32 SIMT
+    otherwise or with --comb-kernel simt) on one of workload.COMB_CONFIGS."""
     import torch
 
     import paper_1802_05427_b200 as ce
@@ -700,6 +701,8 @@ def run_comb(args):
     m_lo, m_hi = antenna_shard(world * cfg.M, world, rank)
     y = workload.comb_instances(cfg, x=x, m_lo=m_lo, m_hi=m_hi)
     est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    est.set_kernel(args.comb_kernel)
+    tc = est.selected_kernel() == ce.CE_COMB_KERNEL_TC
     T, M, N = y.shape
     out_bytes = T * M * cfg.n_ue * N * 8
     nbuf = max(2, int(np.ceil(1.25 * L2_BYTES / (y.nbytes + out_bytes))) + 1)
@@ -743,20 +746,25 @@ def run_comb(args):
     peaks = _peaks()
     hbm_bw = peaks.get("hbm_gbs", 6548.8) * 1e9
     alg_bytes = out_bytes + y.nbytes + x.nbytes
+    # K10: the step is two kernels (k10_ls, k10_comb_tc); the fraction is taken over the whole step
     roof = {"bound": "hbm", "achieved": alg_bytes / kernel_s / 1e9, "peak": hbm_bw / 1e9, "unit": "GB/s",
             "frac": alg_bytes / kernel_s / hbm_bw, "peak_source": "MEASURED_PEAKS hbm_gbs", "traffic": None,
-            "kernel": "k6_estimate", "kernel_us": kernel_s * 1e6, "algorithmic_bytes_per_launch": alg_bytes,
-            "algorithmic_flops_per_launch": 8.0 * cfg.G * E}
+            "kernel": "k10_ls + k10_comb_tc (whole step)" if tc else "k6_estimate_g" if cfg.S == 12 else "k6_estimate",
+            "kernel_us": kernel_s * 1e6, "algorithmic_bytes_per_launch": alg_bytes,
+            "algorithmic_flops_per_launch": 8.0 * cfg.G * E,
+            "alu_bound_us_simt": 8.0 * cfg.G * E / (peaks.get("fp32_tflops", 69.13) * 1e12) * 1e6}
     if rank == 0:
         line = {
             "metric": "channel estimates/s (antenna*user*subcarrier)", "value": value, "unit": "estimates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c64 I/O, fp32 FFMA2 products, fp32 accumulate",
+            "dtype": ("c64 I/O, bf16x3 (error-compensated) tensor products, fp32 accumulate" if tc
+                      else "c64 I/O, fp32 FFMA2 products, fp32 accumulate"),
             "data": "synthetic (workload.comb: Table III channel, fixed-design r_d / SNR_fixed)",
             "config": {"workload": f"comb_{cfg.name}_{cfg.M}x{cfg.n_ue}of{cfg.S}x{cfg.N}_T{cfg.T}_G{cfg.G}_{cfg.mode}",
                        "M": cfg.M, "S": cfg.S, "n_ue": cfg.n_ue, "N": cfg.N, "T": cfg.T, "G": cfg.G,
-                       "mode": cfg.mode, "l2": f"rotating {nbuf} y/h buffer pairs (> L2)",
+                       "mode": cfg.mode, "kernel": "k10_comb_tc (tcgen05)" if tc else "k6 (fp32 simt)",
+                       "l2": f"rotating {nbuf} y/h buffer pairs (> L2)",
                        "parallelism": f"antenna shard x{world}"},
             "roofline": roof, "cpu_baseline": None,
             "e2e": {"value": e2e_value, "unit": "estimates/s", "h2d_bytes_per_step": int(y.nbytes),
@@ -880,6 +888,8 @@ def main():
                          "M antennas per rank; a strong-scaled record of the same configuration rides along at N > 1)")
     ap.add_argument("--stats", action="store_true", help="time the NEXT-3 statistics estimator instead")
     ap.add_argument("--comb", default=None, help="run the comb-pilot 3W/12W path on workload.COMB_CONFIGS[NAME]")
+    ap.add_argument("--comb-kernel", choices=["auto", "simt", "tc"], default="auto",
+                    help="comb estimator kernel: auto (K10 tcgen05 for 12W shapes), simt (K6b), tc (K10)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -193,7 +193,7 @@ int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out);
 /* K6a: FP64 Cholesky build of every (UE, type) weight, rounded to complex64; synchronises the stream
  * once to read the positive-definite flag (CE_ENOTPD). */
 int ce_comb_build_filters(ce_comb_handle *h, void *stream);
-/* K6b hot path on device pointers, asynchronous on `stream`:
+/* Hot path on device pointers (K10, or K6b: ce_comb_set_kernel), asynchronous on `stream`:
  *   d_y : complex64 [T][M][N]     received pilot OFDM symbol of each antenna (all UEs on their combs)
  *   d_x : complex64 [T][N]        comb pilot symbol: tone k carries UE (k % S)'s pilot
  *   d_h : complex64 [T][M][n_ue][N] estimates (caller-owned, must not alias d_y / d_x)
@@ -204,8 +204,18 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
 /* Copy the weights to host: complex64 [n_w][G types][n_out][G], n_w = n_ue (FULL) or 1 (SUB),
  * n_out = S (FULL) or G (SUB).  Synchronous. */
 int ce_comb_get_filters(ce_comb_handle *h, void *host_W);
-/* Kernels launched by this handle (K6a + K6b). */
+/* Kernels launched by this handle (K6a + K6b / K10). */
 int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out);
+/* Estimator kernel of ce_comb_estimate.  AUTO (default): K10 -- the 12W on tcgen05 (BF16x3 products, FP32
+ * accumulation; LS de-interleaved per UE by k10_ls, then one GEMM per (UE, block of groups, 128 rows)) -- whenever
+ * mode == CE_COMB_FULL and G <= 13, else K6b (FP32 SIMT).  SIMT forces K6b; TC forces K10 (CE_EINVAL when the shape
+ * is not supported).  K10 keeps a per-handle device workspace for the LS planes (2 * n_ue * T*M * ceil4(N/S) * 4
+ * bytes), grown on the first call that needs more (a cudaMalloc outside any stream order, so a handle's calls must
+ * not overlap on different streams). */
+typedef enum { CE_COMB_KERNEL_AUTO = 0, CE_COMB_KERNEL_SIMT = 1, CE_COMB_KERNEL_TC = 2 } ce_comb_kernel;
+int ce_comb_set_kernel(ce_comb_handle *h, int32_t kernel);
+/* The kernel the next ce_comb_estimate will use (CE_COMB_KERNEL_SIMT or CE_COMB_KERNEL_TC). */
+int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t *out);
 /* Free; NULL allowed. */
 int ce_comb_free(ce_comb_handle *h);
 

@@ -5,6 +5,9 @@ ctypes binding with the same function names.  No CPU fallback, no oracle import.
 """
 from .ce import (  # noqa: F401
     CE_COMB_FULL,
+    CE_COMB_KERNEL_AUTO,
+    CE_COMB_KERNEL_SIMT,
+    CE_COMB_KERNEL_TC,
     CE_COMB_SUB,
     CE_EINVAL,
     CE_ENODEV,

@@ -32,8 +32,10 @@ EXPORTED = ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "c
             "ce_selected_kernel",
             "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_status_string", "ce_last_error",
             "ce_version", "ce_comb_init", "ce_comb_build_filters", "ce_comb_estimate", "ce_comb_get_filters",
-            "ce_comb_launch_count", "ce_comb_free", "ce_stats_workspace_bytes", "ce_stats_estimate")
+            "ce_comb_launch_count", "ce_comb_set_kernel", "ce_comb_selected_kernel", "ce_comb_free",
+            "ce_stats_workspace_bytes", "ce_stats_estimate")
 CE_COMB_FULL, CE_COMB_SUB = 0, 1
+CE_COMB_KERNEL_AUTO, CE_COMB_KERNEL_SIMT, CE_COMB_KERNEL_TC = 0, 1, 2
 
 
 class ce_params(ctypes.Structure):
@@ -53,6 +55,8 @@ lib.ce_comb_estimate.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32
 lib.ce_comb_get_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_comb_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
 lib.ce_comb_free.argtypes = [c_void_p]
+lib.ce_comb_set_kernel.argtypes = [c_void_p, c_int32]
+lib.ce_comb_selected_kernel.argtypes = [c_void_p, POINTER(c_int32)]
 lib.ce_stats_workspace_bytes.argtypes = [c_int32, c_int32, c_int32, c_int32, POINTER(c_int64)]
 lib.ce_stats_estimate.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int32,
                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
@@ -78,7 +82,8 @@ for _n in ("ce_init", "ce_build_filters", "ce_estimate", "ce_estimate_host", "ce
            "ce_set_kernel",
            "ce_selected_kernel",
            "ce_get_filters", "ce_window_table", "ce_launch_count", "ce_comb_init", "ce_comb_build_filters",
-           "ce_comb_estimate", "ce_comb_get_filters", "ce_comb_launch_count", "ce_comb_free"):
+           "ce_comb_estimate", "ce_comb_get_filters", "ce_comb_launch_count", "ce_comb_set_kernel",
+           "ce_comb_selected_kernel", "ce_comb_free"):
     getattr(lib, _n).restype = c_int
 
 
@@ -352,8 +357,26 @@ class CombEstimator:
             raise ValueError(f"shape mismatch: y {tuple(y.shape)}, x {tuple(x.shape)}, N={self.N}")
         if out is None:
             out = torch.empty((T, M, self.n_ue, N), dtype=torch.complex64, device=y.device)
+        elif (out.dtype != torch.complex64 or out.device != y.device or not out.is_contiguous()
+              or tuple(out.shape) != (T, M, self.n_ue, N)):
+            raise ValueError(f"out must be a contiguous complex64 tensor of shape {(T, M, self.n_ue, N)} on "
+                             f"{y.device}")
+        if x.device != y.device:
+            raise ValueError("y and x must be on the same device")
         ce_comb_estimate(self.handle, y.data_ptr(), x.data_ptr(), out.data_ptr(), T, M, _stream_ptr(stream))
         return out
+
+    def set_kernel(self, kernel) -> "CombEstimator":
+        """CE_COMB_KERNEL_AUTO / _SIMT (K6b) / _TC (K10), or "auto" / "simt" / "tc"."""
+        if isinstance(kernel, str):
+            kernel = {"auto": CE_COMB_KERNEL_AUTO, "simt": CE_COMB_KERNEL_SIMT, "tc": CE_COMB_KERNEL_TC}[kernel]
+        _check(lib.ce_comb_set_kernel(self.handle, int(kernel)), "ce_comb_set_kernel")
+        return self
+
+    def selected_kernel(self) -> int:
+        v = c_int32()
+        _check(lib.ce_comb_selected_kernel(self.handle, ctypes.byref(v)), "ce_comb_selected_kernel")
+        return v.value
 
     def launch_count(self) -> int:
         v = c_int64()

@@ -304,6 +304,14 @@ struct ce_comb_handle {
   float2 *d_W = nullptr;
   int32_t *d_flag = nullptr;
   int64_t launches = 0;
+  // K10 (tcgen05 12W): block table, weight images, LS-plane workspace
+  int kernel = CE_COMB_KERNEL_AUTO;
+  bool tc_ok = false;
+  int n_blk = 0;
+  int4 *d_blk = nullptr;
+  uint16_t *d_img = nullptr;      // [hi | lo] images
+  void *d_ls = nullptr;
+  size_t ls_bytes = 0;
 };
 
 namespace {
@@ -317,6 +325,15 @@ int ccuda(cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? CE_ENOMEM : CE_ECUDA;
 }
 size_t filt_elems(const ce::CombGeo &g) { return size_t(g.n_ue_f) * g.G * g.n_out * g.G; }
+bool use_tc(const ce_comb_handle *h) { return h->tc_ok && h->kernel != CE_COMB_KERNEL_SIMT; }
+void free_comb(ce_comb_handle *h) {
+  cudaFree(h->d_r);
+  cudaFree(h->d_W);
+  cudaFree(h->d_flag);
+  cudaFree(h->d_blk);
+  cudaFree(h->d_img);
+  cudaFree(h->d_ls);
+}
 
 }  // namespace
 
@@ -358,11 +375,17 @@ int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out) {
   if (e == cudaSuccess) e = cudaMalloc(&h->d_W, filt_elems(h->g) * sizeof(float2));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_flag, sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemcpy(h->d_r, p->r_hh, size_t(need) * sizeof(double2), cudaMemcpyHostToDevice);
+  h->tc_ok = ce::comb_tc_supported(p->N, p->S, p->G, p->mode);
+  if (e == cudaSuccess && h->tc_ok) {
+    const std::vector<int4> blk = ce::comb_tc_blocks(K, p->G, p->S);
+    h->n_blk = int(blk.size());
+    e = cudaMalloc(&h->d_blk, blk.size() * sizeof(int4));
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_blk, blk.data(), blk.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_img, 2 * ce::comb_tc_image_elems(p->n_ue, h->n_blk) * sizeof(uint16_t));
+  }
   if (e != cudaSuccess) {
     int st = ccuda(e, "ce_comb_init");
-    cudaFree(h->d_r);
-    cudaFree(h->d_W);
-    cudaFree(h->d_flag);
+    free_comb(h);
     delete h;
     return st;
   }
@@ -387,6 +410,14 @@ int ce_comb_build_filters(ce_comb_handle *h, void *stream) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return ccuda(e, "ce_comb_build_filters: synchronize");
   if (flag) return cfail(CE_ENOTPD, "ce_comb_build_filters: R_pp + sigma^2 I not positive definite");
+  if (h->tc_ok) {                                     // K10 weight images from the complex64 weights
+    const size_t ie = ce::comb_tc_image_elems(h->g.n_ue, h->n_blk);
+    e = ce::launch_comb_tc_images(h->d_W, h->d_blk, h->n_blk, h->g.n_ue, h->g.N, h->g.S, h->g.G, h->d_img,
+                                  h->d_img + ie, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return ccuda(e, "ce_comb_build_filters: K10 images");
+    ++h->launches;
+  }
   h->built = true;
   return CE_OK;
 }
@@ -412,6 +443,22 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float2 *yp = static_cast<const float2 *>(d_y), *xp = static_cast<const float2 *>(d_x);
   float2 *hp = static_cast<float2 *>(d_h);
+  if (use_tc(h)) {
+    const size_t need = ce::comb_tc_ls_bytes(g.N, g.S, g.n_ue, (long long)rows);
+    if (need > h->ls_bytes) {                         // grow the LS-plane workspace (ce.h: outside stream order)
+      cudaFree(h->d_ls);
+      h->d_ls = nullptr;
+      h->ls_bytes = 0;
+      cudaError_t e = cudaMalloc(&h->d_ls, need);
+      if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: K10 workspace");
+      h->ls_bytes = need;
+    }
+    cudaError_t e = ce::launch_comb_tc(yp, xp, hp, T, M, g.N, g.S, g.n_ue, h->d_blk, h->n_blk, h->d_img,
+                                       h->d_img + ce::comb_tc_image_elems(g.n_ue, h->n_blk), h->d_ls, st,
+                                       &h->launches);
+    if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: K10 launch");
+    return CE_OK;
+  }
   const bool spec = g.S == 12 && ((g.mode == CE_COMB_FULL && g.G == 12) || (g.mode == CE_COMB_SUB && g.G == 3));
   const size_t smem_g = (size_t(g.G) * g.n_out * g.G + size_t(ce::RB) * g.K +
                          size_t(ce::RB) * (g.mode == CE_COMB_FULL ? size_t(g.n_out) * (g.K + 1) : size_t(g.K) * g.G)) *
@@ -458,13 +505,27 @@ int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out) {
   return CE_OK;
 }
 
+int ce_comb_set_kernel(ce_comb_handle *h, int32_t kernel) {
+  if (h == nullptr) return cfail(CE_EINVAL, "ce_comb_set_kernel: NULL handle");
+  if (kernel != CE_COMB_KERNEL_AUTO && kernel != CE_COMB_KERNEL_SIMT && kernel != CE_COMB_KERNEL_TC)
+    return cfail(CE_EINVAL, "ce_comb_set_kernel: unknown kernel");
+  if (kernel == CE_COMB_KERNEL_TC && !h->tc_ok)
+    return cfail(CE_EINVAL, "ce_comb_set_kernel: K10 needs mode FULL, G <= 13 and the TMA encoder");
+  h->kernel = kernel;
+  return CE_OK;
+}
+
+int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t *out) {
+  if (h == nullptr || out == nullptr) return cfail(CE_EINVAL, "ce_comb_selected_kernel: NULL argument");
+  *out = use_tc(h) ? CE_COMB_KERNEL_TC : CE_COMB_KERNEL_SIMT;
+  return CE_OK;
+}
+
 int ce_comb_free(ce_comb_handle *h) {
   if (h == nullptr) return CE_OK;
   {
     ce::DeviceGuard dg(h->device);
-    cudaFree(h->d_r);
-    cudaFree(h->d_W);
-    cudaFree(h->d_flag);
+    free_comb(h);
   }
   delete h;
   return CE_OK;

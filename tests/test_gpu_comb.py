@@ -13,9 +13,14 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 
 
-def _run(cfg, y, x, r, s2):
+def _run(cfg, y, x, r, s2, kernel="auto"):
     import paper_1802_05427_b200 as ce
     est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    est.set_kernel(kernel)
+    # AUTO takes K10 (tcgen05) for every 12W-style shape (full mode, G <= 13), K6b otherwise
+    tc_shape = cfg.mode == "full" and cfg.G <= 13
+    want = ce.CE_COMB_KERNEL_SIMT if kernel == "simt" or not tc_shape else ce.CE_COMB_KERNEL_TC
+    assert est.selected_kernel() == want
     h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
     W = est.filters()
@@ -28,14 +33,15 @@ def _rel(h, ref):
     return np.linalg.norm(d, axis=1) / np.linalg.norm(ref.reshape(ref.shape[0], -1), axis=1)
 
 
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
 @pytest.mark.parametrize("name", ["comb_tiny12", "comb_tiny3", "comb_small12", "comb_small3", "paper_12w",
                                   "paper_3w"])
-def test_comb_parity_full(name):
+def test_comb_parity_full(name, kernel):
     cfg = workload.get_comb_config(name)
     r, s2 = workload.comb_stats(cfg)
     x = workload.comb_pilots(cfg)
     y = workload.comb_instances(cfg, x=x)
-    h, W = _run(cfg, y, x, r, s2)
+    h, W = _run(cfg, y, x, r, s2, kernel)
     ref = oracle.comb_estimate(y, x, r, s2, cfg.N, cfg.S, cfg.G, cfg.mode, cfg.n_ue)
     assert np.all(_rel(h, ref) <= TOL), _rel(h, ref)
     # weights: FP64 build, complex64 rounding only
@@ -45,13 +51,14 @@ def test_comb_parity_full(name):
         assert np.linalg.norm(Wg - Wo) / np.linalg.norm(Wo) < 1e-6, (s, typ)
 
 
-def test_comb_massive_sampled():
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
+def test_comb_massive_sampled(kernel):
     """massive_12w (the comb bench workload) at full size in one launch; sampled antennas vs the oracle."""
     cfg = workload.get_comb_config("massive_12w")
     r, s2 = workload.comb_stats(cfg)
     x = workload.comb_pilots(cfg)
     y = workload.comb_instances(cfg, x=x)
-    h, _ = _run(cfg, y, x, r, s2)
+    h, _ = _run(cfg, y, x, r, s2, kernel)
     rng = np.random.default_rng(11)
     for m in rng.choice(cfg.M, size=3, replace=False):
         ref = oracle.comb_estimate(y[:, m:m + 1], x, r, s2, cfg.N, cfg.S, cfg.G, cfg.mode, cfg.n_ue)
@@ -62,8 +69,12 @@ def test_comb_massive_sampled():
 @pytest.mark.parametrize("N,S,n_ue,G,mode", [(60, 6, 6, 10, "full"),     # G = K: one window, full LMMSE
                                              (60, 6, 2, 1, "full"),      # G = 1: scalar Wiener per group
                                              (48, 6, 3, 6, "sub"),       # 3W-like with G = S (1 tone step)
-                                             (64, 8, 5, 2, "sub")])      # ragged n_ue, ZOH step 4
-def test_comb_edge_shapes(N, S, n_ue, G, mode):
+                                             (64, 8, 5, 2, "sub"),       # ragged n_ue, ZOH step 4
+                                             (640, 64, 3, 10, "full"),   # S = 64: one group per K10 block
+                                             (390, 3, 2, 13, "full"),    # G = 13: the widest K10 window
+                                             (520, 4, 4, 14, "full")])   # G = 14: AUTO falls back to K6b
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
+def test_comb_edge_shapes(N, S, n_ue, G, mode, kernel):
     cfg = workload.CombConfig("edge", M=3, S=S, n_ue=n_ue, N=N, Nfft=128, T=2, G=G, mode=mode,
                               tap_delays=(0, 1.5, 3), tap_db=(-1, -5, -9), snr_db=12.0, L_assumed=5.0,
                               snr_fixed_db=25.0)
@@ -71,7 +82,7 @@ def test_comb_edge_shapes(N, S, n_ue, G, mode):
     rng = np.random.default_rng(N + G)
     x = (np.exp(2j * np.pi * rng.random((2, N))) * 1.3).astype(np.complex64)      # non-unit pilots
     y = workload.comb_instances(cfg, x=x)
-    h, _ = _run(cfg, y, x, r, s2)
+    h, _ = _run(cfg, y, x, r, s2, kernel)
     ref = oracle.comb_estimate(y, x, r, s2, N, S, G, mode, n_ue)
     assert np.all(_rel(h, ref) <= TOL)
     if G == N // S and mode == "full":
@@ -100,4 +111,53 @@ def test_comb_errors_zero_and_not_pd():
     with pytest.raises(ce.CEError) as e:
         est.build()
     assert e.value.status == ce.CE_ENOTPD
+    est.close()
+
+
+def _row_rel(h, ref):
+    """max over (instance, antenna, UE) of the relative error of one estimated row (N tones)."""
+    d = np.linalg.norm((h.astype(np.complex128) - ref), axis=-1)
+    return np.max(d / np.maximum(np.linalg.norm(ref, axis=-1), 1e-30))
+
+
+@pytest.mark.parametrize("T,M", [(3, 50), (1, 1), (2, 129), (5, 64)])
+def test_comb_tc_ragged_rows(T, M):
+    """K10 with T*M not a multiple of its 128-row tile (ragged last tile, rows of the next UE inside the TMA box),
+    one row, and exactly two tiles: equal to the oracle per instance (1e-4) and per row (1e-3), and to K6b."""
+    cfg = dataclasses.replace(workload.get_comb_config("comb_small12"), T=T, M=M)
+    r, s2 = workload.comb_stats(cfg)
+    x = workload.comb_pilots(cfg)
+    y = workload.comb_instances(cfg, x=x)
+    h_tc, _ = _run(cfg, y, x, r, s2, "tc")
+    h_simt, _ = _run(cfg, y, x, r, s2, "simt")
+    ref = oracle.comb_estimate(y, x, r, s2, cfg.N, cfg.S, cfg.G, cfg.mode, cfg.n_ue)
+    assert np.all(_rel(h_tc, ref) <= TOL)
+    assert _row_rel(h_tc, ref) <= 1e-3
+    assert np.all(_rel(h_tc, h_simt.astype(np.complex128)) <= TOL)
+
+
+def test_comb_tc_deterministic_and_rejects():
+    """K10 is bitwise repeatable across calls and workspace growth; forcing it on a 3W shape is CE_EINVAL."""
+    import paper_1802_05427_b200 as ce
+    cfg = workload.get_comb_config("paper_12w")
+    r, s2 = workload.comb_stats(cfg)
+    x = torch.from_numpy(workload.comb_pilots(cfg)).cuda()
+    y = torch.from_numpy(workload.comb_instances(cfg, x=x.cpu().numpy())).cuda()
+    est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    h1 = est.estimate(y[:2], x[:2]).clone()            # small workspace first, then a larger call
+    h2 = est.estimate(y, x)
+    h3 = est.estimate(y, x)
+    torch.cuda.synchronize()
+    assert torch.equal(h2, h3)
+    assert torch.equal(h1, h2[:2])
+    n0 = est.launch_count()
+    est.estimate(y, x)
+    assert est.launch_count() == n0 + 2                # k10_ls + k10_comb_tc
+    est.close()
+    cfg3 = workload.get_comb_config("paper_3w")
+    est = ce.CombEstimator(cfg3.N, cfg3.S, cfg3.n_ue, cfg3.G, cfg3.mode, r, s2)
+    with pytest.raises(ce.CEError) as e:
+        est.set_kernel("tc")
+    assert e.value.status == ce.CE_EINVAL
+    assert est.selected_kernel() == ce.CE_COMB_KERNEL_SIMT
     est.close()
