@@ -88,15 +88,16 @@ cudaError_t launch_spectrum_lags(const float2 *y, const float2 *x, int32_t T, in
                                  cudaStream_t stream);
 
 // K10: the comb-pilot 12W (CE_COMB_FULL) on tcgen05 (k10_comb_tc.cu).  Blocks {g0, ng, sw, 0}: ng consecutive
-// groups from g0 whose pilot windows lie in [sw, sw + 16), sw % 4 == 0, ng * S <= 64.
+// groups from g0 whose pilot windows lie in [sw, sw + 16), sw % 4 == 0, ng * S <= 64; cls = the block's weight-image
+// class (blocks with the same groups-per-block, types and tap offsets share one image); rep[cls] = a block of it.
 bool comb_tc_supported(int32_t N, int32_t S, int32_t G, int32_t mode);
-std::vector<int4> comb_tc_blocks(int32_t K, int32_t G, int32_t S);
-size_t comb_tc_image_elems(int32_t n_ue, int32_t n_blk);
+std::vector<int4> comb_tc_blocks(int32_t K, int32_t G, int32_t S, std::vector<int4> *rep);
+size_t comb_tc_image_elems(int32_t n_ue, int32_t n_cls);
 size_t comb_tc_ls_bytes(int32_t N, int32_t S, int32_t n_ue, long long rows);
-cudaError_t launch_comb_tc_images(const float2 *W, const int4 *d_blk, int32_t n_blk, int32_t n_ue, int32_t N,
+cudaError_t launch_comb_tc_images(const float2 *W, const int4 *d_rep, int32_t n_cls, int32_t n_ue, int32_t N,
                                   int32_t S, int32_t G, uint16_t *img_hi, uint16_t *img_lo, cudaStream_t stream);
 cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t T, int32_t M, int32_t N, int32_t S,
-                           int32_t n_ue, const int4 *d_blk, int32_t n_blk, const uint16_t *img_hi,
+                           int32_t n_ue, const int4 *d_blk, int32_t n_blk, int32_t n_cls, const uint16_t *img_hi,
                            const uint16_t *img_lo, void *ls, cudaStream_t stream, int64_t *launches);
 
 void set_last_error(const std::string &msg);

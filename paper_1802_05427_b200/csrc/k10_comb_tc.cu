@@ -33,6 +33,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ce_internal.h"
@@ -47,35 +48,38 @@ constexpr int K10_NR = 128;                 // data rows per unit (MMA N)
 constexpr int K10_PLANE = 128 * 64;         // [128 rows][32 bf16], SW64: 8 KB
 constexpr int K10_SA = 2;                   // weight-image slots
 #ifndef K10_SB_STAGES
-#define K10_SB_STAGES 6
+#define K10_SB_STAGES 4
 #endif
 constexpr int K10_SB = K10_SB_STAGES;       // LS-tile ring
-#ifndef K10_EPI_WARPS
-#define K10_EPI_WARPS 8
-#endif
-constexpr int K10_EPI = K10_EPI_WARPS;      // 4 or 8 epilogue warps (two per TMEM lane quadrant)
+constexpr int K10_EPI = 8;                  // epilogue warps: two per TMEM lane quadrant, two column blocks each
 constexpr int K10_THREADS = 32 * (2 + K10_EPI);
-constexpr int K10_SMEM = (K10_SA + K10_SB) * 2 * K10_PLANE + 256 + 1024;
-static_assert(K10_EPI == 4 || K10_EPI == 8, "K10 epilogue warps");
-static_assert(K10_SMEM <= 232448, "K10 shared memory");
+constexpr int K10_STG = 4096;               // TMA-store staging box [32 rows][32 floats]; two per epilogue warp
+constexpr int K10_MAXBLK = 256;             // block table entries kept in shared memory (else read from global)
+constexpr int K10_SMEM = (K10_SA + K10_SB) * 2 * K10_PLANE + K10_EPI * 2 * K10_STG + 256 + 1024;
+static_assert(K10_SMEM <= 232448 - K10_MAXBLK * 16, "K10 shared memory");
 
 struct K10Params {
   float *h;                     // [T*M][n_ue][N] complex64 as floats
-  const uint16_t *img_hi;       // [n_ue][n_blk][128][32] bf16, SW64 image
+  const uint16_t *img_hi;       // [n_ue][n_cls][128][32] bf16, SW64 image (blocks with equal tap patterns share one)
   const uint16_t *img_lo;
-  const int4 *blk;              // [n_blk] {g0, ng, sw, 0}
-  int R, n_ue, N, S, n_blk, n_rt, u_total;
+  const int4 *blk;              // [n_blk] {g0, ng, sw, image class}
+  int R, n_ue, N, S, n_blk, n_cls, n_rt, u_total;
+  int tma_st;                   // 1: full 32-float quadrant rows leave through staging + 3-D TMA stores
+  int l2_hint;                  // bit 0: LS tiles loaded evict_last (each is re-read by ~4 overlapping windows)
 };
 
 struct Unit10 {
-  int s, b, rt, key;
+  int s, b, rt;
 };
+// units in (row tile, UE, block) order, blocks fastest: a CTA fills consecutive 480-byte output segments of the same
+// 128 rows, so each row's DRAM pages are complete in L2 long before they are written back (rows-fastest order
+// scattered every row's segments over the whole kernel and wrote partial pages)
 __device__ __forceinline__ Unit10 decode10(const K10Params &p, int u) {
   Unit10 d;
-  d.rt = u % p.n_rt;
-  d.key = u / p.n_rt;           // s * n_blk + b: the weight image
-  d.b = d.key % p.n_blk;
-  d.s = d.key / p.n_blk;
+  d.b = u % p.n_blk;
+  const int rest = u / p.n_blk;
+  d.s = rest % p.n_ue;
+  d.rt = rest / p.n_ue;
   return d;
 }
 
@@ -87,50 +91,121 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo_addr, float hi_addr) {
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 
-// LS at every tone of data row r (Eq. 9), scattered into the per-UE bf16 hi / lo planes:
-// plane[(s * R + r) * KP4 + p] = (re, im) of LS at tone S*p + s.  One CTA per row (grid-stride).
-__global__ void __launch_bounds__(256) k10_ls(const float2 *__restrict__ y, const float2 *__restrict__ x,
-                                              uint32_t *__restrict__ ls_hi, uint32_t *__restrict__ ls_lo, int M,
-                                              int R, int N, int S, int n_ue, int KP, int KP4) {
-  extern __shared__ float2 lsrow[];                 // [N]
+// k10_ls: LS at every tone (Eq. 9) of K10_LSR consecutive data rows per CTA, scattered into the
+// per-UE bf16 hi / lo planes: plane[(s * R + r) * KP4 + p] = (re, im) of LS at tone S*p + s (pilots KP .. KP4-1
+// zero).  Phase 1 streams the rows as float4 (two tones) with K10_LSJ independent loads per thread in flight and
+// scatters LS into shared memory as [row][UE][pilot] (odd pilot pitch: consecutive tones land on distinct banks);
+// the (row, tone) and (pilot, UE) coordinates advance by additions only.  Phase 2 writes one plane row per warp
+// (128-byte stores).  N even and 16-byte aligned y / x (else the host takes K6b).
+constexpr int K10_LSR = 6;                  // rows per CTA: R / 6 CTAs at 3 per SM is one wave for massive_12w
+constexpr int K10_LSJ = 4;                  // float4 loads in flight per thread
+constexpr int K10_LST = 256;                // threads
+__device__ __forceinline__ float rcp_ftz(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__global__ void __launch_bounds__(K10_LST) k10_ls(const float4 *__restrict__ y, const float4 *__restrict__ x,
+                                                  uint32_t *__restrict__ ls_hi, uint32_t *__restrict__ ls_lo, int M,
+                                                  int R, int N, int S, int n_ue, int KP, int KP4) {
+  extern __shared__ float2 lst[];                   // [K10_LSR][n_ue][KPS]
   pdl_wait();                                       // y, x (caller data) and the planes (read by the previous call)
+#ifndef K10_LS_LATE_TRIGGER
   if (threadIdx.x == 0) pdl_launch_dependents();    // k10_comb_tc may start its weight-image loads
-  for (int r = blockIdx.x; r < R; r += gridDim.x) {
-    const int t = r / M;
-    const float2 *yr = y + size_t(r) * N;
-    const float2 *xr = x + size_t(t) * N;
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      const float2 yv = yr[k], xv = __ldg(xr + k);
-      const float inv = 1.0f / (xv.x * xv.x + xv.y * xv.y);
-      lsrow[k] = make_float2((yv.x * xv.x + yv.y * xv.y) * inv, (yv.y * xv.x - yv.x * xv.y) * inv);
+#endif
+  const int KPS = KP4 + 1, N2 = N >> 1, t = threadIdx.x;
+  const int rb = blockIdx.x * K10_LSR;
+  const int nr = min(K10_LSR, R - rb);
+  const int tot = nr * N2;                          // float4 (tone pairs) of the CTA's rows
+  // coordinates of float4 i = t: row, tone pair k2 (tone k = 2 k2), pilot pp and UE ss of tone k
+  int row = t / N2, k2 = t - (t / N2) * N2;
+  int pp = (2 * k2) / S, ss = 2 * k2 - pp * S;
+  const int d2 = K10_LST % N2, drow = K10_LST / N2;           // step of (row, k2) per K10_LST float4
+  const int dq = (2 * d2) / S, dr = 2 * d2 - dq * S;           // tone step 2*d2 as (pilots, UEs)
+  const float4 *yb = y + size_t(rb) * N2;
+  const int t0 = rb / M, split = (t0 + 1) * M - rb;  // rows >= split belong to later instances (no division before)
+  for (int i0 = t; i0 < tot; i0 += K10_LSJ * K10_LST) {
+    float4 yv[K10_LSJ], xv[K10_LSJ];
+    int rr[K10_LSJ], kk[K10_LSJ], pq[K10_LSJ], sq[K10_LSJ];
+#pragma unroll
+    for (int j = 0; j < K10_LSJ; ++j) {
+      rr[j] = row;
+      kk[j] = k2;
+      pq[j] = pp;
+      sq[j] = ss;
+      if (i0 + j * K10_LST < tot) {
+        yv[j] = yb[i0 + j * K10_LST];
+        xv[j] = __ldg(x + size_t(row < split ? t0 : (rb + row) / M) * N2 + k2);
+      }
+      // advance by K10_LST float4: the tone moves by 2*d2 (and to the next row drow + carry times)
+      k2 += d2;
+      row += drow;
+      pp += dq;
+      ss += dr;
+      if (ss >= S) {
+        ss -= S;
+        ++pp;
+      }
+      if (k2 >= N2) {
+        k2 -= N2;
+        ++row;
+        pp -= KP;                                   // tone k - N: N = KP * S
+      }
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < n_ue * KP; e += blockDim.x) {
-      const int s = e / KP, p = e - s * KP;
-      const float2 v = lsrow[S * p + s];
-      const uint32_t hi = pack_bf16x2(v.x, v.y);
-      const uint32_t lo = pack_bf16x2(v.x - bf16lo(hi), v.y - bf16hi(hi));
-      const size_t idx = (size_t(s) * R + r) * KP4 + p;
-      ls_hi[idx] = hi;
-      ls_lo[idx] = lo;
+#pragma unroll
+    for (int j = 0; j < K10_LSJ; ++j) {
+      if (i0 + j * K10_LST < tot) {
+        const float i0f = rcp_ftz(xv[j].x * xv[j].x + xv[j].y * xv[j].y);
+        const float i1f = rcp_ftz(xv[j].z * xv[j].z + xv[j].w * xv[j].w);
+        const float f0r = xv[j].x * i0f, f0i = -xv[j].y * i0f, f1r = xv[j].z * i1f, f1i = -xv[j].w * i1f;
+        float2 *base = lst + size_t(rr[j]) * n_ue * KPS;
+        if (sq[j] < n_ue)
+          base[sq[j] * KPS + pq[j]] = make_float2(yv[j].x * f0r - yv[j].y * f0i, yv[j].x * f0i + yv[j].y * f0r);
+        int p1 = pq[j], s1 = sq[j] + 1;             // tone k + 1
+        if (s1 == S) {
+          s1 = 0;
+          ++p1;
+        }
+        if (s1 < n_ue)
+          base[s1 * KPS + p1] = make_float2(yv[j].z * f1r - yv[j].w * f1i, yv[j].z * f1i + yv[j].w * f1r);
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
+  // phase 2: for each UE the CTA's nr plane rows are one contiguous run of nr * KP4 words per plane; thread t owns
+  // words t, t + K10_LST, ... of every UE's run (row / pilot split once), so the UE loop is address increments only
+  const int W = nr * KP4;
+  const size_t ue_step = size_t(R) * KP4;
+  for (int w = t; w < W; w += K10_LST) {
+    const int r = w / KP4, p = w - r * KP4;
+    const bool live = p < KP;
+    const float2 *src = lst + r * n_ue * KPS + p;
+    uint32_t *dh = ls_hi + size_t(rb) * KP4 + w, *dl = ls_lo + size_t(rb) * KP4 + w;
+    for (int sc = 0; sc < n_ue; ++sc, src += KPS, dh += ue_step, dl += ue_step) {
+      const float2 v = live ? *src : make_float2(0.f, 0.f);
+      const uint32_t hv = pack_bf16x2(v.x, v.y);
+      *dh = hv;
+      *dl = pack_bf16x2(v.x - bf16lo(hv), v.y - bf16hi(hv));
+    }
+  }
+#ifdef K10_LS_LATE_TRIGGER
+  if (threadIdx.x == 0) pdl_launch_dependents();
+#endif
 }
 
 // Weight image of (UE s, block b): A[m][kk], m = 2o + c (output o = i*S + q of group g0 + i, c = re / im row),
 // kk = 2j' + c' (pilot sw + j'): the 2x2 real embedding of W_s^(type_g)[q][sw + j' - a_g] (zero outside the
 // group's G taps and beyond the block's outputs); bf16 hi / lo planes in the SW64 image (row m at m*64 bytes,
 // 16-byte chunk (kk/8) ^ ((m>>1)&3)).
-__global__ void k10_build_images(const float2 *__restrict__ W, const int4 *__restrict__ blk, int n_blk, int S,
+__global__ void k10_build_images(const float2 *__restrict__ W, const int4 *__restrict__ rep, int n_cls, int S,
                                  int G, int K, int ml, uint16_t *__restrict__ img_hi, uint16_t *__restrict__ img_lo) {
-  const int b = blockIdx.x, s = blockIdx.y;
-  const int4 B = blk[b];
-  uint16_t *hi = img_hi + (size_t(s) * n_blk + b) * 128 * 32;
-  uint16_t *lo = img_lo + (size_t(s) * n_blk + b) * 128 * 32;
+  const int c = blockIdx.x, s = blockIdx.y;
+  const int4 B = rep[c];                             // a block of image class c
+  uint16_t *hi = img_hi + (size_t(s) * n_cls + c) * 128 * 32;
+  uint16_t *lo = img_lo + (size_t(s) * n_cls + c) * 128 * 32;
   for (int e = threadIdx.x; e < 128 * 32; e += blockDim.x) {
     const int m = e / 32, kk = e % 32;
-    const int o = m >> 1, c = m & 1, jj = kk >> 1, cc = kk & 1;
+    const int o = m >> 1, ri = m & 1, jj = kk >> 1, cc = kk & 1;
     float v = 0.f;
     if (o < B.y * S) {
       const int i = o / S, q = o - i * S, g = B.x + i;
@@ -138,7 +213,7 @@ __global__ void k10_build_images(const float2 *__restrict__ W, const int4 *__res
       const int j = B.z + jj - a;
       if (j >= 0 && j < G) {
         const float2 w = W[((size_t(s) * G + (g - a)) * S + q) * G + j];
-        const int sel = (c << 1) | cc;
+        const int sel = (ri << 1) | cc;
         v = sel == 0 ? w.x : sel == 1 ? -w.y : sel == 2 ? w.y : w.x;
       }
     }
@@ -152,12 +227,14 @@ __global__ void k10_build_images(const float2 *__restrict__ W, const int4 *__res
 
 __global__ void __launch_bounds__(K10_THREADS, 1)
     k10_comb_tc(const __grid_constant__ CUtensorMap tml_hi, const __grid_constant__ CUtensorMap tml_lo,
-                const __grid_constant__ K10Params p) {
+                const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K10Params p) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int4 blk_s[K10_MAXBLK];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sa = smem;                                         // [SA][hi | lo]
   uint8_t *sb = smem + K10_SA * 2 * K10_PLANE;                // [SB][hi | lo]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sb + K10_SB * 2 * K10_PLANE);
+  uint8_t *stg = sb + K10_SB * 2 * K10_PLANE;                 // [EPI warps][2][32 rows][32 floats]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(stg + K10_EPI * 2 * K10_STG);
   uint64_t *a_full = bars, *a_empty = bars + K10_SA;
   uint64_t *b_full = bars + 2 * K10_SA, *b_empty = b_full + K10_SB;
   uint64_t *tmem_full = b_empty + K10_SB, *tmem_empty = tmem_full + 2;
@@ -166,6 +243,9 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int u0 = int((long long)blockIdx.x * p.u_total / gridDim.x);
   const int u1 = int((long long)(blockIdx.x + 1) * p.u_total / gridDim.x);
+  const bool blk_in_smem = p.n_blk <= K10_MAXBLK;
+  if (blk_in_smem)
+    for (int i = tid; i < p.n_blk; i += blockDim.x) blk_s[i] = p.blk[i];   // built by ce_comb_init (not caller data)
   if (tid == 0) {
     for (int i = 0; i < K10_SA; ++i) {
       mbar_init(&a_full[i], 1);
@@ -187,25 +267,29 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tid == 0) pdl_launch_dependents();
+  auto block_of = [&](int b) { return blk_in_smem ? blk_s[b] : __ldg(&p.blk[b]); };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer (TMA / bulk copies)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tml_hi)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tml_lo)) : "memory");
+      const uint64_t pol = l2_evict_last_policy();
       int key_prev = -1, na = 0, ib = 0;
       bool waited = false;
       for (int u = u0; u < u1; ++u, ++ib) {
         const Unit10 d = decode10(p, u);
-        if (d.key != key_prev) {                       // the weight image changes: next A slot
+        const int4 B = block_of(d.b);
+        const int key = d.s * p.n_cls + B.w;           // weight image of (UE, class)
+        if (key != key_prev) {                         // the weight image changes: next A slot
           const int sl = na % K10_SA;
           mbar_wait(&a_empty[sl], ((na / K10_SA) & 1) ^ 1);
           mbar_arrive_expect_tx(&a_full[sl], 2 * K10_PLANE);
-          const size_t src = size_t(d.key) * 128 * 32;
+          const size_t src = size_t(key) * 128 * 32;
           bulk_g2s(sa + sl * 2 * K10_PLANE, p.img_hi + src, K10_PLANE, &a_full[sl]);
           bulk_g2s(sa + sl * 2 * K10_PLANE + K10_PLANE, p.img_lo + src, K10_PLANE, &a_full[sl]);
           ++na;
-          key_prev = d.key;
+          key_prev = key;
         }
         if (!waited) {                                 // the LS planes come from the preceding k10_ls
           pdl_wait();
@@ -214,10 +298,14 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
         const int st = ib % K10_SB;
         mbar_wait(&b_empty[st], ((ib / K10_SB) & 1) ^ 1);
         mbar_arrive_expect_tx(&b_full[st], 2 * K10_PLANE);
-        const int4 B = __ldg(&p.blk[d.b]);
         const int c0 = 2 * B.z, c1 = d.s * p.R + d.rt * K10_NR;
-        tma_load_2d(sb + st * 2 * K10_PLANE, &tml_hi, c0, c1, &b_full[st]);
-        tma_load_2d(sb + st * 2 * K10_PLANE + K10_PLANE, &tml_lo, c0, c1, &b_full[st]);
+        if (p.l2_hint & 1) {
+          tma_load_2d_hint(sb + st * 2 * K10_PLANE, &tml_hi, c0, c1, &b_full[st], pol);
+          tma_load_2d_hint(sb + st * 2 * K10_PLANE + K10_PLANE, &tml_lo, c0, c1, &b_full[st], pol);
+        } else {
+          tma_load_2d(sb + st * 2 * K10_PLANE, &tml_hi, c0, c1, &b_full[st]);
+          tma_load_2d(sb + st * 2 * K10_PLANE + K10_PLANE, &tml_lo, c0, c1, &b_full[st]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -226,12 +314,19 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
       // F32 accumulate, BF16 A / B, both K-major, N = 128, M = 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(K10_NR >> 3) << 17) | (uint32_t(128 >> 4) << 24);
       int key_prev = -1, na = 0, ib = 0, lt = 0;
+      int key_next = u0 < u1 ? decode10(p, u0).s * p.n_cls + block_of(decode10(p, u0).b).w : -1;
       for (int u = u0; u < u1; ++u, ++ib, ++lt) {
-        const Unit10 d = decode10(p, u);
-        if (d.key != key_prev) {
+        const int key = key_next;
+        if (key != key_prev) {
           mbar_wait(&a_full[na % K10_SA], (na / K10_SA) & 1);
           ++na;
-          key_prev = d.key;
+          key_prev = key;
+        }
+        if (u + 1 < u1) {
+          const Unit10 dn = decode10(p, u + 1);
+          key_next = dn.s * p.n_cls + block_of(dn.b).w;
+        } else {
+          key_next = -1;
         }
         const int sl = (na - 1) % K10_SA;
         const int acc = lt & 1;
@@ -252,56 +347,70 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
           mma_bf16(dt, al + adv, bh + adv, idesc, 1u);
         }
         mma_commit(&b_empty[st]);
-        if (u + 1 >= u1 || decode10(p, u + 1).key != d.key) mma_commit(&a_empty[sl]);   // last use of the image
+        if (key_next != key) mma_commit(&a_empty[sl]);   // last use of the image
         mma_commit(&tmem_full[acc]);
       }
     }
   } else {
     // ------------------------------------------------------------------ epilogue
     pdl_wait();                                        // h may still be read by the previous kernel in the stream
+    const int ew = warp - 2;
     const int q = warp & 3;                            // TMEM lane quadrant this warp may access
-    const int part = (warp - 2) >> 2;                  // 8 warps: column blocks {part, part + 2}; 4 warps: all four
-    constexpr int NCB = K10_EPI == 8 ? 2 : 4;
-    const int comp = 32 * q + lane;                    // output float (2o + c) held by this thread
+    const int part = ew >> 2;                          // column blocks {part, part + 2}
+    uint8_t *mystg = stg + ew * 2 * K10_STG;
     const size_t row_floats = size_t(p.n_ue) * p.N * 2;
-    int lt = 0;
+    int lt = 0, nst = 0;
     for (int u = u0; u < u1; ++u, ++lt) {
       const Unit10 d = decode10(p, u);
-      const int4 B = __ldg(&p.blk[d.b]);
+      const int4 B = block_of(d.b);
       const int acc = lt & 1;
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
       tc_fence_after();
-      float v[NCB][32];
+      float v[2][32];
 #pragma unroll
-      for (int i = 0; i < NCB; ++i) {
-        const int cb = K10_EPI == 8 ? part + 2 * i : i;
-        tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * cb) + (uint32_t(32 * q) << 16), v[i]);
-      }
+      for (int i = 0; i < 2; ++i)
+        tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * (part + 2 * i)) + (uint32_t(32 * q) << 16), v[i]);
       __syncwarp();
       if (lane == 0) {
         tc_fence_before();
         mbar_arrive(&tmem_empty[acc]);               // the accumulator is in registers: the MMA may reuse it
       }
-      if (comp < 2 * B.y * p.S) {
-        float *hb = p.h + (size_t(d.s) * p.N + size_t(p.S) * B.x) * 2 + comp;
-        const int rbase = d.rt * K10_NR;
+      const int qc = 2 * B.y * p.S - 32 * q;           // valid output floats in this quadrant
+      const int rbase = d.rt * K10_NR;
+      if (qc >= 32 && p.tma_st) {
+        // staging [32 rows][32 floats] (thread = float, register = row: conflict-free 128-byte rows) -> one 3-D
+        // TMA store of the box {32 floats, UE s, 32 rows}; rows beyond T*M are clipped by the tensor bounds
 #pragma unroll
-        for (int i = 0; i < NCB; ++i) {
-          const int cb = K10_EPI == 8 ? part + 2 * i : i;
-          const int r0 = rbase + 32 * cb;
+        for (int i = 0; i < 2; ++i) {
+          const int r0 = rbase + 32 * (part + 2 * i);
+          if (r0 >= p.R) continue;
+          float *buf = reinterpret_cast<float *>(mystg + (nst & 1) * K10_STG);
+          if (lane == 0) bulk_wait_read1();            // the store that used this buffer has read it
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) buf[c * 32 + lane] = v[i][c];
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmh, buf, 2 * p.S * B.x + 32 * q, d.s, r0);
+            bulk_commit();
+          }
+          ++nst;
+        }
+      } else if (qc > 0 && lane < qc) {
+        float *hb = p.h + (size_t(d.s) * p.N + size_t(p.S) * B.x) * 2 + 32 * q + lane;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r0 = rbase + 32 * (part + 2 * i);
           const int nr = min(32, p.R - r0);
           float *hr = hb + size_t(r0) * row_floats;
-          if (nr >= 32) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) hr[size_t(c) * row_floats] = v[i][c];
-          } else {
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (c < nr) hr[size_t(c) * row_floats] = v[i][c];
-          }
+          for (int c = 0; c < 32; ++c)
+            if (c < nr) hr[size_t(c) * row_floats] = v[i][c];
         }
       }
     }
+    if (lane == 0) bulk_wait0();                       // every TMA store of this warp has completed
   }
   tc_fence_before();
   __syncthreads();
@@ -323,6 +432,19 @@ bool make_map_ls(CUtensorMap *m, const void *ptr, int KP, int KP4, long long row
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// h [R][n_ue][2N floats] as a 3-D tensor (2N, n_ue, R), box {32 floats, 1, 32 rows}, no swizzle (store map).
+bool make_map_h(CUtensorMap *m, const void *ptr, int N, int n_ue, long long R) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t(2) * N, cuuint64_t(n_ue), cuuint64_t(R)};
+  cuuint64_t strides[2] = {cuuint64_t(2) * N * 4, cuuint64_t(2) * N * 4 * n_ue};
+  cuuint32_t box[3] = {32, 1, 32};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -352,40 +474,54 @@ cudaError_t k10_dev(K10Dev **out) {
 
 bool comb_tc_supported(int32_t N, int32_t S, int32_t G, int32_t mode) {
   // a 16-pilot window at a multiple of 4 holds any G <= 13 window; a block's outputs fit M = 128 rows
-  return mode == CE_COMB_FULL && G >= 1 && G <= K10_WIN - 3 && S >= 1 && S <= 64 && N % S == 0 &&
-         encode_fn() != nullptr;
+  // k10_ls stages K10_LSR rows ([n_ue][KP4 + 1] complex each, n_ue <= S) in shared memory and reads float4 (N even)
+  const long long KP4 = S >= 1 ? ((N / S) + 3) & ~3LL : 0;
+  return mode == CE_COMB_FULL && G >= 1 && G <= K10_WIN - 3 && S >= 1 && S <= 64 && N % S == 0 && N % 2 == 0 &&
+         (long long)K10_LSR * S * (KP4 + 1) * 8 <= 200 * 1024 && encode_fn() != nullptr;
 }
 
-std::vector<int4> comb_tc_blocks(int32_t K, int32_t G, int32_t S) {
+std::vector<int4> comb_tc_blocks(int32_t K, int32_t G, int32_t S, std::vector<int4> *rep) {
   const int ml = (G - 1) / 2;
   auto a_of = [&](int g) { return std::min(std::max(g - ml, 0), K - G); };
   const int maxng = 64 / S;
   std::vector<int4> out;
+  std::vector<std::vector<int>> sigs;                // per class: ng, then (type, a - sw) per group
+  rep->clear();
   for (int g = 0; g < K;) {
     const int sw = a_of(g) & ~3;
     int ng = 1;
     while (g + ng < K && ng < maxng && a_of(g + ng) + G <= sw + K10_WIN) ++ng;
-    out.push_back(make_int4(g, ng, sw, 0));
+    std::vector<int> sig{ng};
+    for (int i = 0; i < ng; ++i) {
+      sig.push_back(g + i - a_of(g + i));
+      sig.push_back(a_of(g + i) - sw);
+    }
+    int cls = int(std::find(sigs.begin(), sigs.end(), sig) - sigs.begin());
+    if (cls == int(sigs.size())) {
+      sigs.push_back(sig);
+      rep->push_back(make_int4(g, ng, sw, cls));
+    }
+    out.push_back(make_int4(g, ng, sw, cls));
     g += ng;
   }
   return out;
 }
 
-size_t comb_tc_image_elems(int32_t n_ue, int32_t n_blk) { return size_t(n_ue) * n_blk * 128 * 32; }
+size_t comb_tc_image_elems(int32_t n_ue, int32_t n_cls) { return size_t(n_ue) * n_cls * 128 * 32; }
 
 size_t comb_tc_ls_bytes(int32_t N, int32_t S, int32_t n_ue, long long rows) {
   const long long KP4 = ((N / S) + 3) & ~3LL;
   return size_t(2) * n_ue * rows * KP4 * 4;       // hi and lo planes
 }
 
-cudaError_t launch_comb_tc_images(const float2 *W, const int4 *d_blk, int32_t n_blk, int32_t n_ue, int32_t N,
+cudaError_t launch_comb_tc_images(const float2 *W, const int4 *d_rep, int32_t n_cls, int32_t n_ue, int32_t N,
                                   int32_t S, int32_t G, uint16_t *img_hi, uint16_t *img_lo, cudaStream_t stream) {
-  k10_build_images<<<dim3(n_blk, n_ue), 256, 0, stream>>>(W, d_blk, n_blk, S, G, N / S, (G - 1) / 2, img_hi, img_lo);
+  k10_build_images<<<dim3(n_cls, n_ue), 256, 0, stream>>>(W, d_rep, n_cls, S, G, N / S, (G - 1) / 2, img_hi, img_lo);
   return cudaGetLastError();
 }
 
 cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t T, int32_t M, int32_t N, int32_t S,
-                           int32_t n_ue, const int4 *d_blk, int32_t n_blk, const uint16_t *img_hi,
+                           int32_t n_ue, const int4 *d_blk, int32_t n_blk, int32_t n_cls, const uint16_t *img_hi,
                            const uint16_t *img_lo, void *ls, cudaStream_t stream, int64_t *launches) {
   K10Dev *di = nullptr;
   cudaError_t e = k10_dev(&di);
@@ -404,16 +540,23 @@ cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t 
   // LS planes
   {
     cudaLaunchConfig_t cfg = {};
-    const long long g = R < 8LL * di->num_sms * 4 ? R : 8LL * di->num_sms * 4;
-    cfg.gridDim = dim3(unsigned(g));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = size_t(N) * sizeof(float2);
+    cfg.gridDim = dim3(unsigned((R + K10_LSR - 1) / K10_LSR));
+    cfg.blockDim = dim3(K10_LST);
+    cfg.dynamicSmemBytes = size_t(K10_LSR) * n_ue * (KP4 + 1) * sizeof(float2);
     cfg.stream = stream;
     cfg.attrs = at;
+#ifdef K10_NO_PDL
+    cfg.numAttrs = 0;
+#else
     cfg.numAttrs = 1;
+#endif
     e = smem_opt_in((const void *)k10_ls, cfg.dynamicSmemBytes);
+    // the default carveout left room for 3 CTAs of 39 KB per SM (ncu occupancy limit): ask for the whole array
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k10_ls, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
-    e = cudaLaunchKernelEx(&cfg, k10_ls, y, x, ls_hi, ls_lo, int(M), int(R), int(N), int(S), int(n_ue), KP, KP4);
+    e = cudaLaunchKernelEx(&cfg, k10_ls, reinterpret_cast<const float4 *>(y), reinterpret_cast<const float4 *>(x),
+                           ls_hi, ls_lo, int(M), int(R), int(N), int(S), int(n_ue), KP, KP4);
     if (e != cudaSuccess) return e;
     ++*launches;
   }
@@ -427,18 +570,30 @@ cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t 
   p.N = N;
   p.S = S;
   p.n_blk = n_blk;
+  p.n_cls = n_cls;
   p.n_rt = int((R + K10_NR - 1) / K10_NR);
   const long long units = (long long)n_ue * n_blk * p.n_rt;
   if (units >= (1LL << 31)) return cudaErrorInvalidConfiguration;
   p.u_total = int(units);
+  // 3-D TMA stores need a 16-byte aligned h and 16-byte row pitch (N even); else direct stores
+  static const int env_st = getenv("CE_K10_TMA_STORE") ? atoi(getenv("CE_K10_TMA_STORE")) : -1;   // experiments
+  static const int env_hint = getenv("CE_K10_L2HINT") ? atoi(getenv("CE_K10_L2HINT")) : -1;       // experiments
+  CUtensorMap mhh = {};
+  p.tma_st = env_st != 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (N % 2) == 0 &&
+             make_map_h(&mhh, h, N, n_ue, R);
+  p.l2_hint = env_hint >= 0 ? env_hint : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(units < di->num_sms ? units : di->num_sms));
   cfg.blockDim = dim3(K10_THREADS);
   cfg.dynamicSmemBytes = K10_SMEM;
   cfg.stream = stream;
   cfg.attrs = at;
+#ifdef K10_NO_PDL
+  cfg.numAttrs = 0;
+#else
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k10_comb_tc, mh, ml, p);
+#endif
+  e = cudaLaunchKernelEx(&cfg, k10_comb_tc, mh, ml, mhh, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

@@ -307,8 +307,8 @@ struct ce_comb_handle {
   // K10 (tcgen05 12W): block table, weight images, LS-plane workspace
   int kernel = CE_COMB_KERNEL_AUTO;
   bool tc_ok = false;
-  int n_blk = 0;
-  int4 *d_blk = nullptr;
+  int n_blk = 0, n_cls = 0;
+  int4 *d_blk = nullptr;          // [n_blk] blocks, then [n_cls] class representatives
   uint16_t *d_img = nullptr;      // [hi | lo] images
   void *d_ls = nullptr;
   size_t ls_bytes = 0;
@@ -377,11 +377,14 @@ int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out) {
   if (e == cudaSuccess) e = cudaMemcpy(h->d_r, p->r_hh, size_t(need) * sizeof(double2), cudaMemcpyHostToDevice);
   h->tc_ok = ce::comb_tc_supported(p->N, p->S, p->G, p->mode);
   if (e == cudaSuccess && h->tc_ok) {
-    const std::vector<int4> blk = ce::comb_tc_blocks(K, p->G, p->S);
+    std::vector<int4> rep;
+    std::vector<int4> blk = ce::comb_tc_blocks(K, p->G, p->S, &rep);
     h->n_blk = int(blk.size());
+    h->n_cls = int(rep.size());
+    blk.insert(blk.end(), rep.begin(), rep.end());
     e = cudaMalloc(&h->d_blk, blk.size() * sizeof(int4));
     if (e == cudaSuccess) e = cudaMemcpy(h->d_blk, blk.data(), blk.size() * sizeof(int4), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_img, 2 * ce::comb_tc_image_elems(p->n_ue, h->n_blk) * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_img, 2 * ce::comb_tc_image_elems(p->n_ue, h->n_cls) * sizeof(uint16_t));
   }
   if (e != cudaSuccess) {
     int st = ccuda(e, "ce_comb_init");
@@ -411,8 +414,8 @@ int ce_comb_build_filters(ce_comb_handle *h, void *stream) {
   if (e != cudaSuccess) return ccuda(e, "ce_comb_build_filters: synchronize");
   if (flag) return cfail(CE_ENOTPD, "ce_comb_build_filters: R_pp + sigma^2 I not positive definite");
   if (h->tc_ok) {                                     // K10 weight images from the complex64 weights
-    const size_t ie = ce::comb_tc_image_elems(h->g.n_ue, h->n_blk);
-    e = ce::launch_comb_tc_images(h->d_W, h->d_blk, h->n_blk, h->g.n_ue, h->g.N, h->g.S, h->g.G, h->d_img,
+    const size_t ie = ce::comb_tc_image_elems(h->g.n_ue, h->n_cls);
+    e = ce::launch_comb_tc_images(h->d_W, h->d_blk + h->n_blk, h->n_cls, h->g.n_ue, h->g.N, h->g.S, h->g.G, h->d_img,
                                   h->d_img + ie, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return ccuda(e, "ce_comb_build_filters: K10 images");
@@ -453,8 +456,9 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
       if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: K10 workspace");
       h->ls_bytes = need;
     }
-    cudaError_t e = ce::launch_comb_tc(yp, xp, hp, T, M, g.N, g.S, g.n_ue, h->d_blk, h->n_blk, h->d_img,
-                                       h->d_img + ce::comb_tc_image_elems(g.n_ue, h->n_blk), h->d_ls, st,
+
+    cudaError_t e = ce::launch_comb_tc(yp, xp, hp, T, M, g.N, g.S, g.n_ue, h->d_blk, h->n_blk, h->n_cls, h->d_img,
+                                       h->d_img + ce::comb_tc_image_elems(g.n_ue, h->n_cls), h->d_ls, st,
                                        &h->launches);
     if (e != cudaSuccess) return ccuda(e, "ce_comb_estimate: K10 launch");
     return CE_OK;
