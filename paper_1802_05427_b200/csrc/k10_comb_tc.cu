@@ -9,11 +9,11 @@
 // Formulation.  Groups are packed into blocks of ng consecutive groups whose pilot windows all lie inside one
 // 16-pilot window [sw, sw + 16) with sw a multiple of 4 (host table, comb_tc_blocks; ng * S <= 64 outputs).
 // Per (UE s, block) the block's outputs are one real GEMM
-//     D[2o + c][r] = sum_k  A_s,blk[2o + c][k] * B[r][k],   k = 2j' + c'  (pilot sw + j', re / im)
-// with A the block's weights embedded as 2x2 real blocks [[Re, -Im], [Im, Re]] (rows 2o / 2o + 1 of output o =
-// i*S + q of group g0 + i; zero outside the group's own G taps) and B the LS of UE s at the window's pilots
-// for N = 128 data rows r = (t, m).  M = 128 (<= 64 outputs), N = 128 rows, K = 32 (2 MMA K-steps), BF16x3
-// (A_hi B_hi + A_hi B_lo + A_lo B_hi, FP32 accumulation in TMEM) as K4 (reading B1).
+//     D[r][2o + c] = sum_k  L[r][k] * W_s,blk[2o + c][k],   k = 2j' + c'  (pilot sw + j', re / im)
+// with L the LS of UE s at the window's pilots for M = 128 data rows r = (t, m) and W the block's weights embedded
+// as 2x2 real blocks [[Re, -Im], [Im, Re]] (rows 2o / 2o + 1 of output o = i*S + q of group g0 + i; zero outside the
+// group's own G taps).  M = 128 rows, N = 128 (<= 64 outputs), K = 32 (2 MMA K-steps), BF16x3
+// (L_hi W_hi + L_hi W_lo + L_lo W_hi, FP32 accumulation in TMEM) as K4 (reading B1).
 //
 // Kernels:
 //   k10_ls          LS = y conj(x) / |x|^2 of every tone of a row, de-interleaved per UE into bf16 hi / lo planes
@@ -24,9 +24,9 @@
 //                     warp 0   : producer -- bulk copy of the (UE, block) weight image (pre-swizzled SW64, hi / lo)
 //                                when it changes, 2 TMA loads of the LS tile per unit into a 6-deep ring
 //                     warp 1   : TMEM allocator + MMA issuer (6 MMAs per unit, 2 TMEM accumulators of 128 columns)
-//                     warps 2-9: epilogue -- tcgen05.ld 32x32b: lane = output component, column = data row, so for
-//                                each data row a warp holds 16 consecutive complex outputs and writes them as one
-//                                128-byte coalesced segment of h[t][m][s][.]
+//                     warps 2-9: epilogue -- tcgen05.ld 32x32b: lane = data row, column = output float, so each
+//                                thread holds 128 contiguous bytes of h[t][m][s][.]: SW128 staging (16-byte shared
+//                                stores) and 3-D TMA stores
 //   k10_build_images (build time) the weight images from K6a's complex64 W.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -46,11 +46,25 @@ namespace {
 constexpr int K10_WIN = 16;                 // pilots per block window: K = 32 bf16 = one 64-byte SW64 row
 constexpr int K10_NR = 128;                 // data rows per unit (MMA N)
 constexpr int K10_PLANE = 128 * 64;         // [128 rows][32 bf16], SW64: 8 KB
-constexpr int K10_SA = 2;                   // weight-image slots
+#ifndef K10_SA_SLOTS
+#define K10_SA_SLOTS 2
+#endif
+constexpr int K10_SA = K10_SA_SLOTS;        // weight-image slots
 #ifndef K10_SB_STAGES
 #define K10_SB_STAGES 4
 #endif
 constexpr int K10_SB = K10_SB_STAGES;       // LS-tile ring
+// TMEM accumulators in flight: the 6 MMAs of a unit accumulate into one D and run back to back (~1.5 us from issue
+// to commit), so two accumulators capped the kernel at ~0.8 us per unit with no epilogue at all (ablation); four
+// fill the 512 TMEM columns
+#ifndef K10_NACC_N
+#define K10_NACC_N 4
+#endif
+constexpr int K10_NACC = K10_NACC_N;
+#ifndef K10_ONE_COMMIT
+#define K10_ONE_COMMIT 1
+#endif
+static_assert(!K10_ONE_COMMIT || K10_SB_STAGES == K10_NACC_N, "one commit per unit: LS stage i <-> accumulator i");
 constexpr int K10_EPI = 8;                  // epilogue warps: two per TMEM lane quadrant, two column blocks each
 constexpr int K10_THREADS = 32 * (2 + K10_EPI);
 constexpr int K10_STG = 4096;               // TMA-store staging box [32 rows][32 floats]; two per epilogue warp
@@ -65,8 +79,23 @@ struct K10Params {
   const int4 *blk;              // [n_blk] {g0, ng, sw, image class}
   int R, n_ue, N, S, n_blk, n_cls, n_rt, u_total;
   int tma_st;                   // 1: full 32-float quadrant rows leave through staging + 3-D TMA stores
-  int l2_hint;                  // bit 0: LS tiles loaded evict_last (each is re-read by ~4 overlapping windows)
+  int l2_hint;                  // (default 3) bit 0: LS tiles loaded evict_last (each is re-read by ~4 overlapping windows);
+                                // bit 1: h TMA stores evict_first (the output stream must not push the LS planes out)
 };
+
+// Optional per-CTA event trace (tools/k10_trace.py builds with -DCE_K10_TRACE; the product build has none)
+#ifdef CE_K10_TRACE
+__device__ unsigned long long *g_k10_trace;
+#define K10TR(slot)                                                                       \
+  do {                                                                                    \
+    const unsigned long long c_ = clock64();                                              \
+    if (g_k10_trace) g_k10_trace[size_t(blockIdx.x) * 1024 + (slot)] = c_;                \
+  } while (0)
+#else
+#define K10TR(slot) \
+  do {              \
+  } while (0)
+#endif
 
 struct Unit10 {
   int s, b, rt;
@@ -237,10 +266,11 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(stg + K10_EPI * 2 * K10_STG);
   uint64_t *a_full = bars, *a_empty = bars + K10_SA;
   uint64_t *b_full = bars + 2 * K10_SA, *b_empty = b_full + K10_SB;
-  uint64_t *tmem_full = b_empty + K10_SB, *tmem_empty = tmem_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  uint64_t *tmem_full = b_empty + K10_SB, *tmem_empty = tmem_full + K10_NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + K10_NACC);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) K10TR(0);
   const int u0 = int((long long)blockIdx.x * p.u_total / gridDim.x);
   const int u1 = int((long long)(blockIdx.x + 1) * p.u_total / gridDim.x);
   const bool blk_in_smem = p.n_blk <= K10_MAXBLK;
@@ -255,13 +285,13 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < K10_NACC; ++i) {
       mbar_init(&tmem_full[i], 1);
       mbar_init(&tmem_empty[i], K10_EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  if (warp == 1) tmem_alloc(tmem_slot, K10_NACC * K10_NR);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -296,8 +326,18 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
           waited = true;
         }
         const int st = ib % K10_SB;
+#if K10_ONE_COMMIT
+        // one commit per unit: stage st was read by the MMAs of unit ib - SB, whose completion is tmem_full[st]
+        if (ib >= K10_SB) mbar_wait(&tmem_full[st], ((ib - K10_SB) / K10_NACC) & 1);
+#else
         mbar_wait(&b_empty[st], ((ib / K10_SB) & 1) ^ 1);
+#endif
+#ifdef K10_ABL_NOLOAD
+        mbar_arrive(&b_full[st]);
+        continue;
+#endif
         mbar_arrive_expect_tx(&b_full[st], 2 * K10_PLANE);
+        if (u - u0 < 40) K10TR(8 + u - u0);
         const int c0 = 2 * B.z, c1 = d.s * p.R + d.rt * K10_NR;
         if (p.l2_hint & 1) {
           tma_load_2d_hint(sb + st * 2 * K10_PLANE, &tml_hi, c0, c1, &b_full[st], pol);
@@ -329,11 +369,14 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
           key_next = -1;
         }
         const int sl = (na - 1) % K10_SA;
-        const int acc = lt & 1;
-        mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+        const int acc = lt % K10_NACC;
+        if (lt < 40) K10TR(168 + lt);
+        mbar_wait(&tmem_empty[acc], ((lt / K10_NACC) & 1) ^ 1);
+        if (lt < 40) K10TR(208 + lt);
         const int st = ib % K10_SB;
         mbar_wait(&b_full[st], (ib / K10_SB) & 1);
         tc_fence_after();
+        if (lt < 40) K10TR(48 + lt);
         const uint32_t dt = tmem_base + uint32_t(acc * K10_NR);
         const uint64_t ah = sw64_desc(smem_u32(sa + sl * 2 * K10_PLANE));
         const uint64_t al = sw64_desc(smem_u32(sa + sl * 2 * K10_PLANE + K10_PLANE));
@@ -342,20 +385,27 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint64_t adv = uint64_t(2 * ks);       // +32 bytes along K
-          mma_bf16(dt, ah + adv, bh + adv, idesc, ks != 0);
-          mma_bf16(dt, ah + adv, bl + adv, idesc, 1u);
-          mma_bf16(dt, al + adv, bh + adv, idesc, 1u);
+          // A = the LS tile (M = 128 data rows), B = the weight image (N = 128 output floats): D[row][float]
+          mma_bf16(dt, bh + adv, ah + adv, idesc, ks != 0);
+          mma_bf16(dt, bh + adv, al + adv, idesc, 1u);
+          mma_bf16(dt, bl + adv, ah + adv, idesc, 1u);
         }
+#if !K10_ONE_COMMIT
         mma_commit(&b_empty[st]);
+#endif
         if (key_next != key) mma_commit(&a_empty[sl]);   // last use of the image
         mma_commit(&tmem_full[acc]);
       }
     }
   } else {
     // ------------------------------------------------------------------ epilogue
+    // TMEM lane = data row, column = output float: tcgen05.ld 32x32b gives each thread 32 consecutive output floats
+    // (128 bytes of h) of its row; full 32-float blocks go through SW128 staging (8 conflict-free 16-byte shared stores
+    // per thread) and one 3-D TMA store {32 floats, UE s, 32 rows}; a block cut by the block's output end (5-group
+    // blocks: 120 floats) leaves through direct 16-byte stores of the valid floats
     pdl_wait();                                        // h may still be read by the previous kernel in the stream
     const int ew = warp - 2;
-    const int q = warp & 3;                            // TMEM lane quadrant this warp may access
+    const int q = warp & 3;                            // TMEM lane quadrant = rows 32q .. 32q + 31 of the unit
     const int part = ew >> 2;                          // column blocks {part, part + 2}
     uint8_t *mystg = stg + ew * 2 * K10_STG;
     const size_t row_floats = size_t(p.n_ue) * p.N * 2;
@@ -363,61 +413,87 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
     for (int u = u0; u < u1; ++u, ++lt) {
       const Unit10 d = decode10(p, u);
       const int4 B = block_of(d.b);
-      const int acc = lt & 1;
-      mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
+      const int acc = lt % K10_NACC;
+      mbar_wait(&tmem_full[acc], (lt / K10_NACC) & 1);
       tc_fence_after();
+      if (tid == 64 && lt < 40) K10TR(88 + lt);
+      const int nf = 2 * B.y * p.S;                    // valid output floats of the block
+#ifdef K10_ABL_NOEPI
+      __syncwarp();
+      if (lane == 0) {
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
+      }
+      continue;
+#endif
       float v[2][32];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
-        tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * (part + 2 * i)) + (uint32_t(32 * q) << 16), v[i]);
+        if (32 * (part + 2 * i) < nf)
+          tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * (part + 2 * i)) + (uint32_t(32 * q) << 16), v[i]);
       __syncwarp();
       if (lane == 0) {
         tc_fence_before();
         mbar_arrive(&tmem_empty[acc]);               // the accumulator is in registers: the MMA may reuse it
       }
-      const int qc = 2 * B.y * p.S - 32 * q;           // valid output floats in this quadrant
-      const int rbase = d.rt * K10_NR;
-      if (qc >= 32 && p.tma_st) {
-        // staging [32 rows][32 floats] (thread = float, register = row: conflict-free 128-byte rows) -> one 3-D
-        // TMA store of the box {32 floats, UE s, 32 rows}; rows beyond T*M are clipped by the tensor bounds
+      if (tid == 64 && lt < 40) K10TR(256 + lt);
+      const int r0 = d.rt * K10_NR + 32 * q;           // first row of this warp
+      const int row = r0 + lane;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r0 = rbase + 32 * (part + 2 * i);
-          if (r0 >= p.R) continue;
-          float *buf = reinterpret_cast<float *>(mystg + (nst & 1) * K10_STG);
+      for (int i = 0; i < 2; ++i) {
+        const int cb = part + 2 * i;
+        const int f0 = 32 * cb;
+        if (f0 >= nf || r0 >= p.R) continue;
+        if (f0 + 32 <= nf && p.tma_st) {
+          uint8_t *buf = mystg + (nst & 1) * K10_STG;
           if (lane == 0) bulk_wait_read1();            // the store that used this buffer has read it
           __syncwarp();
+          if (tid == 64 && lt < 40) K10TR(296 + 40 * i + lt);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) buf[c * 32 + lane] = v[i][c];
+          for (int j = 0; j < 8; ++j)                  // SW128: 16-byte chunk j of row `lane` at chunk j ^ (lane & 7)
+            *reinterpret_cast<float4 *>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[i][4 * j], v[i][4 * j + 1], v[i][4 * j + 2], v[i][4 * j + 3]);
+          if (tid == 64 && lt < 40) K10TR(376 + 40 * i + lt);
           fence_proxy_async();
           __syncwarp();
+          if (tid == 64 && lt < 40) K10TR(456 + 40 * i + lt);
           if (lane == 0) {
-            tma_store_3d(&tmh, buf, 2 * p.S * B.x + 32 * q, d.s, r0);
+#ifndef K10_ABL_NOSTORE
+            if (p.l2_hint & 2)
+              tma_store_3d_hint(&tmh, buf, 2 * p.S * B.x + f0, d.s, r0, l2_evict_first_policy());
+            else
+              tma_store_3d(&tmh, buf, 2 * p.S * B.x + f0, d.s, r0);
+#endif
             bulk_commit();
           }
           ++nst;
-        }
-      } else if (qc > 0 && lane < qc) {
-        float *hb = p.h + (size_t(d.s) * p.N + size_t(p.S) * B.x) * 2 + 32 * q + lane;
+        } else if (row < p.R) {
+          float *hr = p.h + size_t(row) * row_floats + (size_t(d.s) * p.N + size_t(p.S) * B.x) * 2 + f0;
+          const int nv = min(32, nf - f0);             // a multiple of 4 (2 S ng floats, S * ng even)
+          if ((reinterpret_cast<uintptr_t>(hr) & 15) == 0 && (nv & 3) == 0) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r0 = rbase + 32 * (part + 2 * i);
-          const int nr = min(32, p.R - r0);
-          float *hr = hb + size_t(r0) * row_floats;
+            for (int j = 0; j < 8; ++j)
+              if (4 * j < nv)
+                *reinterpret_cast<float4 *>(hr + 4 * j) =
+                    make_float4(v[i][4 * j], v[i][4 * j + 1], v[i][4 * j + 2], v[i][4 * j + 3]);
+          } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c < nr) hr[size_t(c) * row_floats] = v[i][c];
+            for (int c = 0; c < 32; ++c)
+              if (c < nv) hr[c] = v[i][c];
+          }
         }
       }
+      if (tid == 64 && lt < 40) K10TR(128 + lt);
     }
     if (lane == 0) bulk_wait0();                       // every TMA store of this warp has completed
+    if (tid == 64) K10TR(1);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, 256);
+    tmem_dealloc(tmem_base, K10_NACC * K10_NR);
   }
 }
 
@@ -435,7 +511,7 @@ bool make_map_ls(CUtensorMap *m, const void *ptr, int KP, int KP4, long long row
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// h [R][n_ue][2N floats] as a 3-D tensor (2N, n_ue, R), box {32 floats, 1, 32 rows}, no swizzle (store map).
+// h [R][n_ue][2N floats] as a 3-D tensor (2N, n_ue, R), box {32 floats, 1, 32 rows}, SWIZZLE_128B (store map).
 bool make_map_h(CUtensorMap *m, const void *ptr, int N, int n_ue, long long R) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
@@ -444,7 +520,7 @@ bool make_map_h(CUtensorMap *m, const void *ptr, int N, int n_ue, long long R) {
   cuuint32_t box[3] = {32, 1, 32};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -471,6 +547,10 @@ cudaError_t k10_dev(K10Dev **out) {
 }
 
 }  // namespace
+
+#ifdef CE_K10_TRACE
+extern "C" int ce_k10_trace_set(void *dptr) { return int(cudaMemcpyToSymbol(g_k10_trace, &dptr, sizeof(dptr))); }
+#endif
 
 bool comb_tc_supported(int32_t N, int32_t S, int32_t G, int32_t mode) {
   // a 16-pilot window at a multiple of 4 holds any G <= 13 window; a block's outputs fit M = 128 rows
@@ -581,7 +661,8 @@ cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t 
   CUtensorMap mhh = {};
   p.tma_st = env_st != 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (N % 2) == 0 &&
              make_map_h(&mhh, h, N, n_ue, R);
-  p.l2_hint = env_hint >= 0 ? env_hint : 1;
+  // evict_last LS loads + evict_first h stores: the LS planes stay in L2 (DRAM reads 23 -> 1.3 MB per launch)
+  p.l2_hint = env_hint >= 0 ? env_hint : 3;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(units < di->num_sms ? units : di->num_sms));
   cfg.blockDim = dim3(K10_THREADS);
