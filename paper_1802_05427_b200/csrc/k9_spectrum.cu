@@ -20,9 +20,11 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "ce_internal.h"
+#include "tc_ptx.cuh"
 
 namespace ce {
 namespace {
@@ -202,13 +204,18 @@ struct K9Shape {
 };
 
 // P[set][f] += sum over this CTA's rows of |X_row[f]|^2.  CTA = (instance t, rows [g cpb, (g + 1) cpb)).
-template <int LOG2L>
+// PF (N even, 16-byte aligned y): each team's y rows are bulk-copied (cp.async.bulk, one mbarrier per stage) into a
+// 2-stage shared-memory ring two rows ahead, so pass 0 reads shared memory instead of waiting on DRAM (ncu, config 4
+// without it: long_scoreboard 37 % of the stall samples, FMA pipe 50 %)
+template <int LOG2L, bool PF>
 __global__ void __launch_bounds__(K9Shape<LOG2L>::NT, K9Shape<LOG2L>::NT >= 512 ? 1 : 2) k9_spectrum(const float2 *__restrict__ y, const float2 *__restrict__ x,
                                                                    int M, int K, int N, const int32_t *__restrict__ soi,
                                                                    int n_sets, int cpb, double *__restrict__ P) {
   using S = K9Shape<LOG2L>;
   constexpr int L = S::L, TEAM = S::TEAM, TEAMS = S::TEAMS;
   extern __shared__ float2 sm9[];
+  float2 *ystg = sm9 + TEAMS * S::LP;                       // PF: [TEAMS][2][N] y rows
+  uint64_t *ybar = reinterpret_cast<uint64_t *>(ystg + (PF ? size_t(TEAMS) * 2 * N : 0));   // PF: [TEAMS][2]
   const int MK = M * K;
   const int groups = (MK + cpb - 1) / cpb;
   const int t = blockIdx.x / groups, g = blockIdx.x % groups;
@@ -220,13 +227,36 @@ __global__ void __launch_bounds__(K9Shape<LOG2L>::NT, K9Shape<LOG2L>::NT >= 512 
   float acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-  for (int c0 = c_lo; c0 < c_hi; c0 += TEAMS) {
+  const uint32_t ybytes = uint32_t(N) * 8u;
+  if constexpr (PF) {
+    if (jt == 0) {
+      mbar_init(&ybar[2 * team], 1);
+      mbar_init(&ybar[2 * team + 1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        const int cr = c_lo + st * TEAMS + team;
+        if (cr < c_hi) {
+          mbar_arrive_expect_tx(&ybar[2 * team + st], ybytes);
+          bulk_g2s(ystg + (2 * team + st) * N, y + (size_t(t) * MK + cr) * N, ybytes, &ybar[2 * team + st]);
+        }
+      }
+    }
+    __syncthreads();                                        // barriers initialised before any team waits on them
+  }
+  int it = 0;
+  for (int c0 = c_lo; c0 < c_hi; c0 += TEAMS, ++it) {
     const int c = c0 + team;
     const bool ok = c < c_hi;
     float2 v[16];
-    // pass 0 (radix 16, Ns = 1): LS values straight from global memory, zero beyond N and for absent rows
+    // pass 0 (radix 16, Ns = 1): LS values from global memory (PF: y from the team's ring), zero beyond N and for
+    // absent rows
     {
       const float2 *yr = y + (size_t(t) * MK + (ok ? c : c_lo)) * N;
+      if constexpr (PF) {
+        yr = ystg + (2 * team + (it & 1)) * N;
+        if (ok) mbar_wait(&ybar[2 * team + (it & 1)], (it >> 1) & 1);
+      }
       const float2 *xr = x + (size_t(t) * K + (ok ? c : c_lo) % K) * N;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -245,6 +275,13 @@ __global__ void __launch_bounds__(K9Shape<LOG2L>::NT, K9Shape<LOG2L>::NT >= 512 
     int lNs = 4;
     pass_store<16, L>(v, buf, jt, 0);
     __syncthreads();
+    if constexpr (PF) {                                     // every thread has read this stage: refill it two rows ahead
+      const int cr = c + 2 * TEAMS;
+      if (jt == 0 && cr < c_hi) {
+        mbar_arrive_expect_tx(&ybar[2 * team + (it & 1)], ybytes);
+        bulk_g2s(ystg + (2 * team + (it & 1)) * N, y + (size_t(t) * MK + cr) * N, ybytes, &ybar[2 * team + (it & 1)]);
+      }
+    }
     // middle radix-16 passes
 #pragma unroll 1
     for (int p = 1; p < S::N16 - (S::RLAST == 1 ? 1 : 0); ++p) {
@@ -323,8 +360,13 @@ template <int LOG2L>
 cudaError_t launch_spectrum_t(const float2 *y, const float2 *x, int T, int M, int K, int N, const int32_t *soi,
                               int n_sets, double *P, cudaStream_t st) {
   using S = K9Shape<LOG2L>;
-  const size_t smem = size_t(S::TEAMS) * S::LP * sizeof(float2);
-  cudaError_t e = smem_opt_in((const void *)k9_spectrum<LOG2L>, smem);
+  static const int env_pf = getenv("CE_K9_PF") ? atoi(getenv("CE_K9_PF")) : 1;   // experiments
+  const size_t smem0 = size_t(S::TEAMS) * S::LP * sizeof(float2);
+  const size_t smem_pf = smem0 + size_t(S::TEAMS) * 2 * N * sizeof(float2) + size_t(S::TEAMS) * 2 * sizeof(uint64_t);
+  const bool pf = env_pf != 0 && N % 2 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && smem_pf <= 220 * 1024;
+  const size_t smem = pf ? smem_pf : smem0;
+  const void *fn = pf ? (const void *)k9_spectrum<LOG2L, true> : (const void *)k9_spectrum<LOG2L, false>;
+  cudaError_t e = smem_opt_in(fn, smem);
   if (e != cudaSuccess) return e;
   int nsm = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -337,7 +379,10 @@ cudaError_t launch_spectrum_t(const float2 *y, const float2 *x, int T, int M, in
   const long long groups = ((long long)M * K + cpb - 1) / cpb;
   const long long ctas = (long long)T * groups;
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  k9_spectrum<LOG2L><<<unsigned(ctas), S::NT, smem, st>>>(y, x, M, K, N, soi, n_sets, int(cpb), P);
+  if (pf)
+    k9_spectrum<LOG2L, true><<<unsigned(ctas), S::NT, smem, st>>>(y, x, M, K, N, soi, n_sets, int(cpb), P);
+  else
+    k9_spectrum<LOG2L, false><<<unsigned(ctas), S::NT, smem, st>>>(y, x, M, K, N, soi, n_sets, int(cpb), P);
   return cudaGetLastError();
 }
 

@@ -1,4 +1,5 @@
 # K10 profile: launch list (per-kernel times) + ncu --set full of k10_comb_tc and k10_ls on massive_12w
+mkdir -p gpurun_out
 TAG=${1:-k10}
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build_${TAG}.log 2>&1 || exit 1
 CMD="python bench.py --comb massive_12w --comb-kernel tc --steps 10 --warmup 3 --e2e-steps 3"

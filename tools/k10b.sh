@@ -1,4 +1,5 @@
 TAG=${1:-k10b}
+mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build_${TAG}.log 2>&1 || { tail -30 gpurun_out/build_${TAG}.log; exit 1; }
 timeout 900 python -m pytest tests/test_gpu_comb.py -q -x 2>&1 | tail -5
 for k in tc; do timeout 300 python bench.py --comb massive_12w --comb-kernel $k --steps 50 --warmup 5 > gpurun_out/comb_${TAG}_$k.json 2> gpurun_out/comb_${TAG}_$k.err; echo "bench $k rc $?"; tail -3 gpurun_out/comb_${TAG}_$k.err; done
