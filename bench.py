@@ -702,8 +702,8 @@ def run_comb(args):
     y = workload.comb_instances(cfg, x=x, m_lo=m_lo, m_hi=m_hi)
     est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
     est.set_kernel(args.comb_kernel)
-    tc = est.selected_kernel() == ce.CE_COMB_KERNEL_TC
     T, M, N = y.shape
+    tc = est.selected_kernel(T, M) == ce.CE_COMB_KERNEL_TC
     out_bytes = T * M * cfg.n_ue * N * 8
     nbuf = max(2, int(np.ceil(1.25 * L2_BYTES / (y.nbytes + out_bytes))) + 1)
     y_dev = [torch.from_numpy(y).to(dev) for _ in range(nbuf)]

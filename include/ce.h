@@ -207,15 +207,17 @@ int ce_comb_get_filters(ce_comb_handle *h, void *host_W);
 /* Kernels launched by this handle (K6a + K6b / K10). */
 int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out);
 /* Estimator kernel of ce_comb_estimate.  AUTO (default): K10 -- the 12W on tcgen05 (BF16x3 products, FP32
- * accumulation; LS de-interleaved per UE by k10_ls, then one GEMM per (UE, block of groups, 128 rows)) -- whenever
- * mode == CE_COMB_FULL and G <= 13, else K6b (FP32 SIMT).  SIMT forces K6b; TC forces K10 (CE_EINVAL when the shape
- * is not supported).  K10 keeps a per-handle device workspace for the LS planes (2 * n_ue * T*M * ceil4(N/S) * 4
- * bytes), grown on the first call that needs more (a cudaMalloc outside any stream order, so a handle's calls must
- * not overlap on different streams). */
+ * accumulation; LS de-interleaved per UE by k10_ls, then one GEMM per (UE, block of groups, 128 rows)) -- when
+ * mode == CE_COMB_FULL, G <= 13, N even and the call has at least 4 units of work per SM
+ * (ceil(T*M / 128) * n_ue * blocks, ~N/(4S) blocks), else K6b (FP32 SIMT; one launch, faster on small calls).  SIMT
+ * forces K6b; TC forces K10 for every call (CE_EINVAL when the shape is not supported).  K10 keeps a per-handle
+ * device workspace for the LS planes (2 * n_ue * T*M * ceil4(N/S) * 4 bytes), grown on the first call that needs
+ * more (a cudaMalloc outside any stream order, so a handle's calls must not overlap on different streams). */
 typedef enum { CE_COMB_KERNEL_AUTO = 0, CE_COMB_KERNEL_SIMT = 1, CE_COMB_KERNEL_TC = 2 } ce_comb_kernel;
 int ce_comb_set_kernel(ce_comb_handle *h, int32_t kernel);
-/* The kernel the next ce_comb_estimate will use (CE_COMB_KERNEL_SIMT or CE_COMB_KERNEL_TC). */
-int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t *out);
+/* The kernel ce_comb_estimate will use for a call with T instances of M antennas (CE_COMB_KERNEL_SIMT or
+ * CE_COMB_KERNEL_TC); CE_EINVAL for T or M < 1. */
+int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t T, int32_t M, int32_t *out);
 /* Free; NULL allowed. */
 int ce_comb_free(ce_comb_handle *h);
 

@@ -56,7 +56,7 @@ lib.ce_comb_get_filters.argtypes = [c_void_p, c_void_p]
 lib.ce_comb_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
 lib.ce_comb_free.argtypes = [c_void_p]
 lib.ce_comb_set_kernel.argtypes = [c_void_p, c_int32]
-lib.ce_comb_selected_kernel.argtypes = [c_void_p, POINTER(c_int32)]
+lib.ce_comb_selected_kernel.argtypes = [c_void_p, c_int32, c_int32, POINTER(c_int32)]
 lib.ce_stats_workspace_bytes.argtypes = [c_int32, c_int32, c_int32, c_int32, POINTER(c_int64)]
 lib.ce_stats_estimate.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int32,
                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
@@ -373,9 +373,10 @@ class CombEstimator:
         _check(lib.ce_comb_set_kernel(self.handle, int(kernel)), "ce_comb_set_kernel")
         return self
 
-    def selected_kernel(self) -> int:
+    def selected_kernel(self, T: int = 1, M: int = 1) -> int:
+        """The kernel an estimate() of T instances x M antennas will use (CE_COMB_KERNEL_SIMT / _TC)."""
         v = c_int32()
-        _check(lib.ce_comb_selected_kernel(self.handle, ctypes.byref(v)), "ce_comb_selected_kernel")
+        _check(lib.ce_comb_selected_kernel(self.handle, int(T), int(M), ctypes.byref(v)), "ce_comb_selected_kernel")
         return v.value
 
     def launch_count(self) -> int:

@@ -50,15 +50,18 @@ constexpr int K10_PLANE = 128 * 64;         // [128 rows][32 bf16], SW64: 8 KB
 #define K10_SA_SLOTS 2
 #endif
 constexpr int K10_SA = K10_SA_SLOTS;        // weight-image slots
+#ifndef K10_CPS
+#define K10_CPS 1
+#endif
 #ifndef K10_SB_STAGES
-#define K10_SB_STAGES 4
+#define K10_SB_STAGES (K10_CPS == 1 ? 4 : 2)
 #endif
 constexpr int K10_SB = K10_SB_STAGES;       // LS-tile ring
 // TMEM accumulators in flight: the 6 MMAs of a unit accumulate into one D and run back to back (~1.5 us from issue
 // to commit), so two accumulators capped the kernel at ~0.8 us per unit with no epilogue at all (ablation); four
 // fill the 512 TMEM columns
 #ifndef K10_NACC_N
-#define K10_NACC_N 4
+#define K10_NACC_N (K10_CPS == 1 ? 4 : 2)
 #endif
 constexpr int K10_NACC = K10_NACC_N;
 #ifndef K10_ONE_COMMIT
@@ -67,9 +70,14 @@ constexpr int K10_NACC = K10_NACC_N;
 static_assert(!K10_ONE_COMMIT || K10_SB_STAGES == K10_NACC_N, "one commit per unit: LS stage i <-> accumulator i");
 constexpr int K10_EPI = 8;                  // epilogue warps: two per TMEM lane quadrant, two column blocks each
 constexpr int K10_THREADS = 32 * (2 + K10_EPI);
-constexpr int K10_STG = 4096;               // TMA-store staging box [32 rows][32 floats]; two per epilogue warp
+constexpr int K10_STG = 4096;               // TMA-store staging box [32 rows][32 floats]
+#ifndef K10_CPS
+#define K10_CPS 1
+#endif
+constexpr int K10_CTAS = K10_CPS;           // CTAs per SM (2: half-size rings, one staging box per epilogue warp)
+constexpr int K10_NSTG = K10_CTAS == 1 ? 2 : 1;   // staging boxes per epilogue warp
 constexpr int K10_MAXBLK = 256;             // block table entries kept in shared memory (else read from global)
-constexpr int K10_SMEM = (K10_SA + K10_SB) * 2 * K10_PLANE + K10_EPI * 2 * K10_STG + 256 + 1024;
+constexpr int K10_SMEM = (K10_SA + K10_SB) * 2 * K10_PLANE + K10_EPI * K10_NSTG * K10_STG + 256 + 1024;
 static_assert(K10_SMEM <= 232448 - K10_MAXBLK * 16, "K10 shared memory");
 
 struct K10Params {
@@ -254,7 +262,7 @@ __global__ void k10_build_images(const float2 *__restrict__ W, const int4 *__res
   }
 }
 
-__global__ void __launch_bounds__(K10_THREADS, 1)
+__global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
     k10_comb_tc(const __grid_constant__ CUtensorMap tml_hi, const __grid_constant__ CUtensorMap tml_lo,
                 const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K10Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
   uint8_t *sa = smem;                                         // [SA][hi | lo]
   uint8_t *sb = smem + K10_SA * 2 * K10_PLANE;                // [SB][hi | lo]
   uint8_t *stg = sb + K10_SB * 2 * K10_PLANE;                 // [EPI warps][2][32 rows][32 floats]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(stg + K10_EPI * 2 * K10_STG);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(stg + K10_EPI * K10_NSTG * K10_STG);
   uint64_t *a_full = bars, *a_empty = bars + K10_SA;
   uint64_t *b_full = bars + 2 * K10_SA, *b_empty = b_full + K10_SB;
   uint64_t *tmem_full = b_empty + K10_SB, *tmem_empty = tmem_full + K10_NACC;
@@ -407,7 +415,7 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
     const int ew = warp - 2;
     const int q = warp & 3;                            // TMEM lane quadrant = rows 32q .. 32q + 31 of the unit
     const int part = ew >> 2;                          // column blocks {part, part + 2}
-    uint8_t *mystg = stg + ew * 2 * K10_STG;
+    uint8_t *mystg = stg + ew * K10_NSTG * K10_STG;
     const size_t row_floats = size_t(p.n_ue) * p.N * 2;
     int lt = 0, nst = 0;
     for (int u = u0; u < u1; ++u, ++lt) {
@@ -445,8 +453,13 @@ __global__ void __launch_bounds__(K10_THREADS, 1)
         const int f0 = 32 * cb;
         if (f0 >= nf || r0 >= p.R) continue;
         if (f0 + 32 <= nf && p.tma_st) {
-          uint8_t *buf = mystg + (nst & 1) * K10_STG;
-          if (lane == 0) bulk_wait_read1();            // the store that used this buffer has read it
+          uint8_t *buf = mystg + (nst % K10_NSTG) * K10_STG;
+          if (lane == 0) {                             // the store that used this buffer has read it
+            if (K10_NSTG == 2)
+              bulk_wait_read1();
+            else
+              bulk_wait_read0();
+          }
           __syncwarp();
           if (tid == 64 && lt < 40) K10TR(296 + 40 * i + lt);
 #pragma unroll
@@ -539,6 +552,8 @@ cudaError_t k10_dev(K10Dev **out) {
     e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k10_comb_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, K10_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k10_comb_tc, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     d.init = true;
   }
@@ -664,7 +679,8 @@ cudaError_t launch_comb_tc(const float2 *y, const float2 *x, float2 *h, int32_t 
   // evict_last LS loads + evict_first h stores: the LS planes stay in L2 (DRAM reads 23 -> 1.3 MB per launch)
   p.l2_hint = env_hint >= 0 ? env_hint : 3;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(units < di->num_sms ? units : di->num_sms));
+  const long long slots = (long long)K10_CTAS * di->num_sms;
+  cfg.gridDim = dim3(unsigned(units < slots ? units : slots));
   cfg.blockDim = dim3(K10_THREADS);
   cfg.dynamicSmemBytes = K10_SMEM;
   cfg.stream = stream;

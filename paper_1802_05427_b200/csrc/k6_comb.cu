@@ -325,7 +325,17 @@ int ccuda(cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? CE_ENOMEM : CE_ECUDA;
 }
 size_t filt_elems(const ce::CombGeo &g) { return size_t(g.n_ue_f) * g.G * g.n_out * g.G; }
-bool use_tc(const ce_comb_handle *h) { return h->tc_ok && h->kernel != CE_COMB_KERNEL_SIMT; }
+// K10 under AUTO only with enough units (128-row tile, UE, block) for ~4 per SM: small calls are latency-bound and two
+// launches (k10_ls + k10_comb_tc) cost more than K6b's one (paper_12w, 1152 (row, UE) pairs: K10 25.4 us, K6b 19.2 us;
+// massive_12w: 76 vs 155 us)
+bool use_tc(const ce_comb_handle *h, long long T, long long M) {
+  if (!h->tc_ok || h->kernel == CE_COMB_KERNEL_SIMT) return false;
+  if (h->kernel == CE_COMB_KERNEL_TC) return true;
+  int dev = h->device, nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long units = ((T * M + 127) / 128) * h->g.n_ue * h->n_blk;
+  return units >= 4LL * nsm;
+}
 void free_comb(ce_comb_handle *h) {
   cudaFree(h->d_r);
   cudaFree(h->d_W);
@@ -446,7 +456,7 @@ int ce_comb_estimate(ce_comb_handle *h, const void *d_y, const void *d_x, void *
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float2 *yp = static_cast<const float2 *>(d_y), *xp = static_cast<const float2 *>(d_x);
   float2 *hp = static_cast<float2 *>(d_h);
-  if (use_tc(h)) {
+  if (use_tc(h, T, M)) {
     const size_t need = ce::comb_tc_ls_bytes(g.N, g.S, g.n_ue, (long long)rows);
     if (need > h->ls_bytes) {                         // grow the LS-plane workspace (ce.h: outside stream order)
       cudaFree(h->d_ls);
@@ -519,9 +529,10 @@ int ce_comb_set_kernel(ce_comb_handle *h, int32_t kernel) {
   return CE_OK;
 }
 
-int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t *out) {
+int ce_comb_selected_kernel(const ce_comb_handle *h, int32_t T, int32_t M, int32_t *out) {
   if (h == nullptr || out == nullptr) return cfail(CE_EINVAL, "ce_comb_selected_kernel: NULL argument");
-  *out = use_tc(h) ? CE_COMB_KERNEL_TC : CE_COMB_KERNEL_SIMT;
+  if (T < 1 || M < 1) return cfail(CE_EINVAL, "ce_comb_selected_kernel: T and M must be >= 1");
+  *out = use_tc(h, T, M) ? CE_COMB_KERNEL_TC : CE_COMB_KERNEL_SIMT;
   return CE_OK;
 }
 

@@ -16,11 +16,15 @@ TOL = 1e-4
 def _run(cfg, y, x, r, s2, kernel="auto"):
     import paper_1802_05427_b200 as ce
     est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    # K10 (tcgen05) serves every 12W-style shape (full mode, G <= 13, N even): "tc" forces it there, "simt" forces K6b;
+    # AUTO takes K10 only for calls with >= 4 units per SM (checked in test_comb_auto_policy)
+    tc_shape = cfg.mode == "full" and cfg.G <= 13 and cfg.N % 2 == 0
+    if kernel == "tc" and not tc_shape:
+        kernel = "auto"
     est.set_kernel(kernel)
-    # AUTO takes K10 (tcgen05) for every 12W-style shape (full mode, G <= 13), K6b otherwise
-    tc_shape = cfg.mode == "full" and cfg.G <= 13
-    want = ce.CE_COMB_KERNEL_SIMT if kernel == "simt" or not tc_shape else ce.CE_COMB_KERNEL_TC
-    assert est.selected_kernel() == want
+    want = ce.CE_COMB_KERNEL_TC if kernel == "tc" else ce.CE_COMB_KERNEL_SIMT if kernel == "simt" else None
+    if want is not None:
+        assert est.selected_kernel(cfg.T, cfg.M) == want
     h = est.estimate(torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
     W = est.filters()
@@ -33,7 +37,7 @@ def _rel(h, ref):
     return np.linalg.norm(d, axis=1) / np.linalg.norm(ref.reshape(ref.shape[0], -1), axis=1)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
 @pytest.mark.parametrize("name", ["comb_tiny12", "comb_tiny3", "comb_small12", "comb_small3", "paper_12w",
                                   "paper_3w"])
 def test_comb_parity_full(name, kernel):
@@ -73,7 +77,7 @@ def test_comb_massive_sampled(kernel):
                                              (640, 64, 3, 10, "full"),   # S = 64: one group per K10 block
                                              (390, 3, 2, 13, "full"),    # G = 13: the widest K10 window
                                              (520, 4, 4, 14, "full")])   # G = 14: AUTO falls back to K6b
-@pytest.mark.parametrize("kernel", ["auto", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
 def test_comb_edge_shapes(N, S, n_ue, G, mode, kernel):
     cfg = workload.CombConfig("edge", M=3, S=S, n_ue=n_ue, N=N, Nfft=128, T=2, G=G, mode=mode,
                               tap_delays=(0, 1.5, 3), tap_db=(-1, -5, -9), snr_db=12.0, L_assumed=5.0,
@@ -143,7 +147,7 @@ def test_comb_tc_deterministic_and_rejects():
     r, s2 = workload.comb_stats(cfg)
     x = torch.from_numpy(workload.comb_pilots(cfg)).cuda()
     y = torch.from_numpy(workload.comb_instances(cfg, x=x.cpu().numpy())).cuda()
-    est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build().set_kernel("tc")
     h1 = est.estimate(y[:2], x[:2]).clone()            # small workspace first, then a larger call
     h2 = est.estimate(y, x)
     h3 = est.estimate(y, x)
@@ -159,5 +163,24 @@ def test_comb_tc_deterministic_and_rejects():
     with pytest.raises(ce.CEError) as e:
         est.set_kernel("tc")
     assert e.value.status == ce.CE_EINVAL
-    assert est.selected_kernel() == ce.CE_COMB_KERNEL_SIMT
+    assert est.selected_kernel(cfg3.T, cfg3.M) == ce.CE_COMB_KERNEL_SIMT
+    est.close()
+
+
+def test_comb_auto_policy():
+    """AUTO: K10 for massive_12w-sized calls (>= 4 units of (128 rows, UE, block) per SM), K6b for small calls and for
+    the 3W; the massive call itself goes through K10 (two launches) and the small one through K6b (one)."""
+    import paper_1802_05427_b200 as ce
+    cfg = workload.get_comb_config("massive_12w")
+    r, s2 = workload.comb_stats(cfg)
+    est = ce.CombEstimator(cfg.N, cfg.S, cfg.n_ue, cfg.G, cfg.mode, r, s2).build()
+    assert est.selected_kernel(cfg.T, cfg.M) == ce.CE_COMB_KERNEL_TC
+    assert est.selected_kernel(1, 16) == ce.CE_COMB_KERNEL_SIMT
+    x = torch.from_numpy(workload.comb_pilots(cfg)).cuda()
+    y = torch.zeros((1, 16, cfg.N), dtype=torch.complex64, device="cuda")
+    n0 = est.launch_count()
+    est.estimate(y, x[:1])
+    assert est.launch_count() == n0 + 1
+    with pytest.raises(ce.CEError):
+        est.selected_kernel(0, 4)
     est.close()

@@ -24,3 +24,15 @@ CMD5="python bench.py --config 5 --launch direct --steps 4 --warmup 3 --no-cpu-b
 eval $CMD5 > gpurun_out/plain5_${TAG}.log 2>&1 && \
   eval ncu --set full --clock-control none --import-source on -k regex:k4_bf16x3 -s 3 -c 1 -f -o gpurun_out/prof_c5_${TAG} $CMD5 > gpurun_out/ncu_full5_${TAG}.log 2>&1
 echo "full c5 rc $?"
+# K10 (comb 12W on tcgen05): launch list and ncu --set full of the main kernel
+CMDC="python bench.py --comb massive_12w --steps 10 --warmup 3 --e2e-steps 3"
+eval $CMDC > gpurun_out/plainc_${TAG}.log 2>&1 && \
+  eval ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none -c 40 --csv --log-file gpurun_out/launches_comb_${TAG}.csv $CMDC > /dev/null 2>&1
+echo "comb launch list rc $?"
+eval ncu --set full --clock-control none --import-source on -k regex:k10_comb_tc -s 3 -c 1 -f -o gpurun_out/prof_k10_${TAG} $CMDC > gpurun_out/ncu_k10_${TAG}.log 2>&1
+echo "full k10 rc $?"
+for c in 4 5; do
+CMDS="python bench.py --stats --config $c --steps 3 --warmup 3"
+eval ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --cache-control none -c 30 --csv --log-file gpurun_out/launches_stats_c${c}_${TAG}.csv $CMDS > /dev/null 2>&1
+echo "stats c$c launch list rc $?"
+done
