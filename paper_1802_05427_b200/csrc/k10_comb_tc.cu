@@ -68,14 +68,18 @@ constexpr int K10_NACC = K10_NACC_N;
 #define K10_ONE_COMMIT 1
 #endif
 static_assert(!K10_ONE_COMMIT || K10_SB_STAGES == K10_NACC_N, "one commit per unit: LS stage i <-> accumulator i");
-constexpr int K10_EPI = 8;                  // epilogue warps: two per TMEM lane quadrant, two column blocks each
+#ifndef K10_EPI_W
+#define K10_EPI_W 8
+#endif
+constexpr int K10_EPI = K10_EPI_W;          // epilogue warps: 8 (two per TMEM lane quadrant, two column blocks each) or 16
+constexpr int K10_NCBW = 16 / K10_EPI;      // 32-float column blocks per epilogue warp and unit
 constexpr int K10_THREADS = 32 * (2 + K10_EPI);
 constexpr int K10_STG = 4096;               // TMA-store staging box [32 rows][32 floats]
 #ifndef K10_CPS
 #define K10_CPS 1
 #endif
 constexpr int K10_CTAS = K10_CPS;           // CTAs per SM (2: half-size rings, one staging box per epilogue warp)
-constexpr int K10_NSTG = K10_CTAS == 1 ? 2 : 1;   // staging boxes per epilogue warp
+constexpr int K10_NSTG = (K10_CTAS == 1 && K10_EPI_W == 8) ? 2 : 1;   // staging boxes per epilogue warp
 constexpr int K10_MAXBLK = 256;             // block table entries kept in shared memory (else read from global)
 constexpr int K10_SMEM = (K10_SA + K10_SB) * 2 * K10_PLANE + K10_EPI * K10_NSTG * K10_STG + 256 + 1024;
 static_assert(K10_SMEM <= 232448 - K10_MAXBLK * 16, "K10 shared memory");
@@ -118,6 +122,17 @@ __device__ __forceinline__ Unit10 decode10(const K10Params &p, int u) {
   d.s = rest % p.n_ue;
   d.rt = rest / p.n_ue;
   return d;
+}
+// the next unit without a division (the issue loops are single-thread latency chains: measured ~0.4 us of
+// instruction overhead per unit with two decodes by division in the MMA issuer)
+__device__ __forceinline__ void next10(const K10Params &p, Unit10 &d) {
+  if (++d.b == p.n_blk) {
+    d.b = 0;
+    if (++d.s == p.n_ue) {
+      d.s = 0;
+      ++d.rt;
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_addr, float hi_addr) {
@@ -315,8 +330,8 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       const uint64_t pol = l2_evict_last_policy();
       int key_prev = -1, na = 0, ib = 0;
       bool waited = false;
-      for (int u = u0; u < u1; ++u, ++ib) {
-        const Unit10 d = decode10(p, u);
+      Unit10 d = decode10(p, u0);
+      for (int u = u0; u < u1; ++u, ++ib, next10(p, d)) {
         const int4 B = block_of(d.b);
         const int key = d.s * p.n_cls + B.w;           // weight image of (UE, class)
         if (key != key_prev) {                         // the weight image changes: next A slot
@@ -362,7 +377,8 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       // F32 accumulate, BF16 A / B, both K-major, N = 128, M = 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(K10_NR >> 3) << 17) | (uint32_t(128 >> 4) << 24);
       int key_prev = -1, na = 0, ib = 0, lt = 0;
-      int key_next = u0 < u1 ? decode10(p, u0).s * p.n_cls + block_of(decode10(p, u0).b).w : -1;
+      Unit10 dn = decode10(p, u0);
+      int key_next = u0 < u1 ? dn.s * p.n_cls + block_of(dn.b).w : -1;
       for (int u = u0; u < u1; ++u, ++ib, ++lt) {
         const int key = key_next;
         if (key != key_prev) {
@@ -371,7 +387,7 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
           key_prev = key;
         }
         if (u + 1 < u1) {
-          const Unit10 dn = decode10(p, u + 1);
+          next10(p, dn);
           key_next = dn.s * p.n_cls + block_of(dn.b).w;
         } else {
           key_next = -1;
@@ -414,12 +430,12 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
     pdl_wait();                                        // h may still be read by the previous kernel in the stream
     const int ew = warp - 2;
     const int q = warp & 3;                            // TMEM lane quadrant = rows 32q .. 32q + 31 of the unit
-    const int part = ew >> 2;                          // column blocks {part, part + 2}
+    const int part = ew >> 2;                          // column blocks part + (K10_EPI / 4) i
     uint8_t *mystg = stg + ew * K10_NSTG * K10_STG;
     const size_t row_floats = size_t(p.n_ue) * p.N * 2;
     int lt = 0, nst = 0;
-    for (int u = u0; u < u1; ++u, ++lt) {
-      const Unit10 d = decode10(p, u);
+    Unit10 d = decode10(p, u0);
+    for (int u = u0; u < u1; ++u, ++lt, next10(p, d)) {
       const int4 B = block_of(d.b);
       const int acc = lt % K10_NACC;
       mbar_wait(&tmem_full[acc], (lt / K10_NACC) & 1);
@@ -434,11 +450,11 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       }
       continue;
 #endif
-      float v[2][32];
+      float v[K10_NCBW][32];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
-        if (32 * (part + 2 * i) < nf)
-          tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * (part + 2 * i)) + (uint32_t(32 * q) << 16), v[i]);
+      for (int i = 0; i < K10_NCBW; ++i)
+        if (32 * (part + (K10_EPI / 4) * i) < nf)
+          tmem_ld32(tmem_base + uint32_t(acc * K10_NR + 32 * (part + (K10_EPI / 4) * i)) + (uint32_t(32 * q) << 16), v[i]);
       __syncwarp();
       if (lane == 0) {
         tc_fence_before();
@@ -448,8 +464,8 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       const int r0 = d.rt * K10_NR + 32 * q;           // first row of this warp
       const int row = r0 + lane;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int cb = part + 2 * i;
+      for (int i = 0; i < K10_NCBW; ++i) {
+        const int cb = part + (K10_EPI / 4) * i;
         const int f0 = 32 * cb;
         if (f0 >= nf || r0 >= p.R) continue;
         if (f0 + 32 <= nf && p.tma_st) {

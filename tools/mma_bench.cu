@@ -219,6 +219,55 @@ __global__ void bench_ts1(int iters, int N, unsigned long long *out) {
   }
 }
 
+// K10 / K4 issue pattern: units of 2 K-steps x 3 products (A_hi B_hi, A_hi B_lo, A_lo B_hi) into one of NACC
+// accumulators, one commit per unit to that accumulator's mbarrier; before unit u the issuer waits for unit u - NACC
+// (the accumulator is free again).  mode 1: additionally wait on unit u - 1's barrier (fully serialised units)
+__global__ void bench_units(int iters, int N, int nacc, int mode, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bars[8];
+  __shared__ uint32_t slot;
+  uint8_t *smem = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t d0 = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    const uint64_t ah = sw64_desc(smem_u32(smem)), al = sw64_desc(smem_u32(smem + 16 * 1024));
+    const uint64_t bh = sw64_desc(smem_u32(smem + 32 * 1024)), bl = sw64_desc(smem_u32(smem + 48 * 1024));
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int acc = it % nacc;
+      if (it >= nacc) mbar_wait(&bars[acc], ((it - nacc) / nacc) & 1);
+      if (mode == 1 && it >= 1) mbar_wait(&bars[(it - 1) % nacc], ((it - 1) / nacc) & 1);
+      tc_fence_after();
+      const uint32_t d = d0 + uint32_t(acc * N);
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint64_t adv = uint64_t(2 * ks);
+        mma_bf16(d, ah + adv, bh + adv, idesc, ks != 0);
+        mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
+        mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+      }
+      mma_commit(&bars[acc]);
+    }
+    for (int it = iters - nacc; it < iters; ++it) if (it >= 0) mbar_wait(&bars[it % nacc], (it / nacc) & 1);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(d0, 512);
+  }
+}
+
 int main() {
   unsigned long long *dout, h[148];
   cudaMalloc(&dout, 148 * 8);
@@ -238,6 +287,20 @@ int main() {
       const double flop = 2.0 * 128 * N * 16;
       printf("N=%3d grid %3d: SW64 %.1f cyc/MMA (%.0f flop/clk)  SW128 %.1f cyc/MMA (%.0f flop/clk)  %s\n", N, grid, c64,
              flop / c64, c128, flop / c128, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  cudaFuncSetAttribute(bench_units, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int N : {128, 256}) {
+    for (int nacc : {1, 2, 4}) {
+      if (nacc * N > 512) continue;
+      for (int mode : {0, 1}) {
+        const int iters = 2048;
+        bench_units<<<148, 128, 100 * 1024>>>(iters, N, nacc, mode, dout);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, dout, 8, cudaMemcpyDeviceToHost);
+        const double c = double(h[0]) / (iters * 6);
+        printf("UNITS N=%3d nacc %d mode %d: %.1f cyc/MMA  %s\n", N, nacc, mode, c, cudaGetErrorString(cudaGetLastError()));
+      }
     }
   }
   cudaFuncSetAttribute(bench_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
