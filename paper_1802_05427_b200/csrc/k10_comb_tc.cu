@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
   if (tid == 0) pdl_launch_dependents();
   auto block_of = [&](int b) { return blk_in_smem ? blk_s[b] : __ldg(&p.blk[b]); };
 
+#ifdef K10_ABL_STOREONLY
+  if (warp < 2) {
+  } else
+#endif
   if (warp == 0) {
     // ------------------------------------------------------------------ producer (TMA / bulk copies)
     if (lane == 0) {
@@ -438,8 +442,10 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
     for (int u = u0; u < u1; ++u, ++lt, next10(p, d)) {
       const int4 B = block_of(d.b);
       const int acc = lt % K10_NACC;
+#ifndef K10_ABL_STOREONLY
       mbar_wait(&tmem_full[acc], (lt / K10_NACC) & 1);
       tc_fence_after();
+#endif
       if (tid == 64 && lt < 40) K10TR(88 + lt);
       const int nf = 2 * B.y * p.S;                    // valid output floats of the block
 #ifdef K10_ABL_NOEPI
@@ -451,6 +457,12 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       continue;
 #endif
       float v[K10_NCBW][32];
+#ifdef K10_ABL_STOREONLY
+#pragma unroll
+      for (int i = 0; i < K10_NCBW; ++i)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[i][c] = float(c + lane);
+#else
 #pragma unroll
       for (int i = 0; i < K10_NCBW; ++i)
         if (32 * (part + (K10_EPI / 4) * i) < nf)
@@ -460,6 +472,7 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
         tc_fence_before();
         mbar_arrive(&tmem_empty[acc]);               // the accumulator is in registers: the MMA may reuse it
       }
+#endif
       if (tid == 64 && lt < 40) K10TR(256 + lt);
       const int r0 = d.rt * K10_NR + 32 * q;           // first row of this warp
       const int row = r0 + lane;
@@ -491,7 +504,11 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
             if (p.l2_hint & 2)
               tma_store_3d_hint(&tmh, buf, 2 * p.S * B.x + f0, d.s, r0, l2_evict_first_policy());
             else
+#ifdef K10_ABL_ALIGNED
+              tma_store_3d(&tmh, buf, ((2 * p.S * B.x) & ~31) + f0, d.s, r0);   // line-aligned (results wrong)
+#else
               tma_store_3d(&tmh, buf, 2 * p.S * B.x + f0, d.s, r0);
+#endif
 #endif
             bulk_commit();
           }
