@@ -47,11 +47,14 @@ constexpr int K10_WIN = 16;                 // pilots per block window: K = 32 b
 constexpr int K10_NR = 128;                 // data rows per unit (MMA N)
 constexpr int K10_PLANE = 128 * 64;         // [128 rows][32 bf16], SW64: 8 KB
 #ifndef K10_SA_SLOTS
-#define K10_SA_SLOTS 2
+#define K10_SA_SLOTS 4       // interleaved units change the weight image almost every unit
 #endif
 constexpr int K10_SA = K10_SA_SLOTS;        // weight-image slots
 #ifndef K10_CPS
 #define K10_CPS 1
+#endif
+#ifndef K10_INTERLEAVE
+#define K10_INTERLEAVE 1     // grid-stride units (measured: 74.3 -> 72.4 us with 4 image slots)
 #endif
 #ifndef K10_SB_STAGES
 #define K10_SB_STAGES (K10_CPS == 1 ? 4 : 2)
@@ -69,7 +72,7 @@ constexpr int K10_NACC = K10_NACC_N;
 #endif
 static_assert(!K10_ONE_COMMIT || K10_SB_STAGES == K10_NACC_N, "one commit per unit: LS stage i <-> accumulator i");
 #ifndef K10_EPI_W
-#define K10_EPI_W 8
+#define K10_EPI_W 16         // measured: 16 warps 71.3 us, 8 warps 72.4 us (interleaved units, 4 image slots)
 #endif
 constexpr int K10_EPI = K10_EPI_W;          // epilogue warps: 8 (two per TMEM lane quadrant, two column blocks each) or 16
 constexpr int K10_NCBW = 16 / K10_EPI;      // 32-float column blocks per epilogue warp and unit
@@ -294,8 +297,16 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) K10TR(0);
+#if K10_INTERLEAVE
+  // grid-stride units: at any moment the CTAs work on consecutive units (the blocks of the same rows and UE), so every
+  // row's output pages are written by many SMs within a short window
+  const int u0 = 0, u1 = (p.u_total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  auto unit_at = [&](int j) { return decode10(p, int(blockIdx.x) + j * int(gridDim.x)); };
+#else
   const int u0 = int((long long)blockIdx.x * p.u_total / gridDim.x);
   const int u1 = int((long long)(blockIdx.x + 1) * p.u_total / gridDim.x);
+  auto unit_at = [&](int j) { return decode10(p, j); };
+#endif
   const bool blk_in_smem = p.n_blk <= K10_MAXBLK;
   if (blk_in_smem)
     for (int i = tid; i < p.n_blk; i += blockDim.x) blk_s[i] = p.blk[i];   // built by ce_comb_init (not caller data)
@@ -334,8 +345,8 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       const uint64_t pol = l2_evict_last_policy();
       int key_prev = -1, na = 0, ib = 0;
       bool waited = false;
-      Unit10 d = decode10(p, u0);
-      for (int u = u0; u < u1; ++u, ++ib, next10(p, d)) {
+      for (int u = u0; u < u1; ++u, ++ib) {
+        const Unit10 d = unit_at(u);
         const int4 B = block_of(d.b);
         const int key = d.s * p.n_cls + B.w;           // weight image of (UE, class)
         if (key != key_prev) {                         // the weight image changes: next A slot
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
       // F32 accumulate, BF16 A / B, both K-major, N = 128, M = 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(K10_NR >> 3) << 17) | (uint32_t(128 >> 4) << 24);
       int key_prev = -1, na = 0, ib = 0, lt = 0;
-      Unit10 dn = decode10(p, u0);
+      Unit10 dn = unit_at(u0);
       int key_next = u0 < u1 ? dn.s * p.n_cls + block_of(dn.b).w : -1;
       for (int u = u0; u < u1; ++u, ++ib, ++lt) {
         const int key = key_next;
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
           key_prev = key;
         }
         if (u + 1 < u1) {
-          next10(p, dn);
+          dn = unit_at(u + 1);
           key_next = dn.s * p.n_cls + block_of(dn.b).w;
         } else {
           key_next = -1;
@@ -438,8 +449,8 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
     uint8_t *mystg = stg + ew * K10_NSTG * K10_STG;
     const size_t row_floats = size_t(p.n_ue) * p.N * 2;
     int lt = 0, nst = 0;
-    Unit10 d = decode10(p, u0);
-    for (int u = u0; u < u1; ++u, ++lt, next10(p, d)) {
+    for (int u = u0; u < u1; ++u, ++lt) {
+      const Unit10 d = unit_at(u);
       const int4 B = block_of(d.b);
       const int acc = lt % K10_NACC;
 #ifndef K10_ABL_STOREONLY
@@ -496,6 +507,22 @@ __global__ void __launch_bounds__(K10_THREADS, K10_CTAS)
             *reinterpret_cast<float4 *>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                 make_float4(v[i][4 * j], v[i][4 * j + 1], v[i][4 * j + 2], v[i][4 * j + 3]);
           if (tid == 64 && lt < 40) K10TR(376 + 40 * i + lt);
+#ifdef K10_ST_LSU
+          // coalesced LSU stores from the staged block: each instruction writes 4 rows x 128 B (full lines)
+          __syncwarp();
+          {
+            float *hb = p.h + (size_t(d.s) * p.N + size_t(p.S) * B.x) * 2 + f0 + 4 * (lane & 7);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rr = 4 * k + (lane >> 3), j = lane & 7;
+              const float4 w = *reinterpret_cast<const float4 *>(buf + rr * 128 + ((j ^ (rr & 7)) << 4));
+              if (r0 + rr < p.R) *reinterpret_cast<float4 *>(hb + size_t(r0 + rr) * row_floats) = w;
+            }
+          }
+          __syncwarp();
+          ++nst;
+          continue;
+#endif
           fence_proxy_async();
           __syncwarp();
           if (tid == 64 && lt < 40) K10TR(456 + 40 * i + lt);
