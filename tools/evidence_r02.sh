@@ -36,3 +36,7 @@ CMDS="python bench.py --stats --config $c --steps 3 --warmup 3"
 eval ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --cache-control none -c 30 --csv --log-file gpurun_out/launches_stats_c${c}_${TAG}.csv $CMDS > /dev/null 2>&1
 echo "stats c$c launch list rc $?"
 done
+# the NCCL plumbing through the driver's launcher (one rank: torch.distributed.run, backend nccl)
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 1 --steps 20 --warmup 5 --sweep "" --no-cpu-baseline > gpurun_out/bench_nccl1_${TAG}.json 2> gpurun_out/bench_nccl1_${TAG}.err
+echo "nccl torchrun rc $?"
