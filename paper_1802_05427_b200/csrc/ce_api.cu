@@ -486,10 +486,14 @@ static int estimate_host_impl(ce_handle *h, const void *y_host, const void *x_ho
   // kernel on a second, every D2H copy on a third, chained per chunk by events -- the host->device and
   // device->host DMA engines each stream back to back and run concurrently (measured 86 GB/s together,
   // 52 GB/s each alone); 4 MB chunks measured best for config 3 (2 MB: -10%,
-  // 1 MB: -20%: per-copy overhead); large batches run at the PCIe duplex ceiling (config 4: 90 GB/s).
+  // 1 MB: -20%: per-copy overhead); large batches run at the PCIe duplex ceiling (config 4: 90 GB/s).  The
+  // asynchronous call overlaps whole calls instead (call n's device->host copies with call n+1's host->device copies,
+  // two staging slots), where fewer, larger copies win: config 3 with 32 MB chunks (one per call) 5.4-5.6e9
+  // estimates/s against 4.1e9 with 4 MB chunks (same box; the synchronous call: 4 MB 3.8e9, 8 MB 3.6e9).
   const size_t ant_bytes = size_t(K) * N * sizeof(float2);
-  static const long env_chunk_kb = getenv("CE_HOST_CHUNK_KB") ? atol(getenv("CE_HOST_CHUNK_KB")) : 4096;   // experiments
-  int32_t m_chunk = int32_t(std::max<size_t>(1, size_t(env_chunk_kb) * 1024 / ant_bytes));
+  static const long env_chunk_kb = getenv("CE_HOST_CHUNK_KB") ? atol(getenv("CE_HOST_CHUNK_KB")) : 0;   // experiments
+  const long chunk_kb = env_chunk_kb > 0 ? env_chunk_kb : sync ? 4096 : 32768;
+  int32_t m_chunk = int32_t(std::max<size_t>(1, size_t(chunk_kb) * 1024 / ant_bytes));
   m_chunk = std::min(m_chunk, M);
   // at most MAX_CHUNKS chunks: fall back to whole instances per chunk, several instances per chunk if needed
   int32_t t_chunk = 1;
