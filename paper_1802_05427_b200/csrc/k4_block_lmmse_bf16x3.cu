@@ -70,7 +70,11 @@ constexpr int RAWY = TM * CK * 8;          // 16 KB
 constexpr int RAWX = KMAX * CK * 8;        // 4 KB
 constexpr int RAW_STAGE = RAWY + RAWX;     // 20 KB
 constexpr int EPI_WARP = 4096;             // TMA-store staging per epilogue warp: [32 rows][128 B], SWIZZLE_128B
-constexpr int EPI_BYTES = 4 * EPI_WARP;
+#ifndef K4_EPI_DB
+#define K4_EPI_DB 0          // experiments: 1 = two staging boxes per epilogue warp (two stores in flight), 2 raw stages
+#endif
+constexpr int EPI_NB = K4_EPI_DB ? 2 : 1;
+constexpr int EPI_BYTES = 4 * EPI_NB * EPI_WARP;
 constexpr int BAR_BYTES = 256;
 constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
 
@@ -81,7 +85,7 @@ constexpr int S_AB = K4_S_AB;              // A/B stages (measured: 4 y + 3 A/B 
 constexpr int B_PLANE = NMAXW * 64;        // 16 KB
 constexpr int AB_STAGE = 2 * A_PLANE + 2 * B_PLANE;      // 48 KB
 // with staging: 3 A/B + 3 raw stages + staging; without: 3 A/B + 4 raw stages
-constexpr int K4_SMEM_ST = S_AB * AB_STAGE + (S_RAW_MAX - 1) * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+constexpr int K4_SMEM_ST = S_AB * AB_STAGE + (S_RAW_MAX - 1 - K4_EPI_DB) * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
 constexpr int K4_SMEM_NOST = S_AB * AB_STAGE + S_RAW_MAX * RAW_STAGE + BAR_BYTES + 1024;
 constexpr int K4_SMEM = K4_SMEM_ST > K4_SMEM_NOST ? K4_SMEM_ST : K4_SMEM_NOST;
 static_assert(K4_SMEM <= 232448, "K4 shared memory");
@@ -162,7 +166,7 @@ __device__ __forceinline__ float rcp_approx(float v) {
 // last tile the A/B ring is idle and every (warp, block) gets its own staging buffer there.
 __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *tmh, uint32_t tmem_base, uint8_t *ab,
                                           uint8_t *epi, const Tile4 &ti, int cb, int q, int lane, int acc, bool last,
-                                          bool set_ok) {
+                                          bool set_ok, int &nst) {
   const int rA = lane >> 2, cq = lane & 3;
   const int nf = 2 * ti.kept;
   // tcgen05.ld 16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row
@@ -173,8 +177,14 @@ __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *
   tmem_ld_wait();
   if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
       ti.ct * TM + q * 32 + 32 <= p.cols) {
-    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + q * EPI_WARP;
-    if (!last && lane == 0) bulk_wait_read0();       // the previous store has read the staging buffer
+    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + (q * EPI_NB + (nst % EPI_NB)) * EPI_WARP;
+    if (!last && lane == 0) {                        // the store that used this staging buffer has read it
+      if (EPI_NB == 2)
+        bulk_wait_read1();
+      else
+        bulk_wait_read0();
+    }
+    if (!last) ++nst;
     __syncwarp();
     const uint32_t nanb = 0x7fc00000u;
 #pragma unroll
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // TMEM -> registers (16x256b: 4 consecutive threads hold 4 consecutive complex outputs of one row)
     // -> direct 8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes.
     const int q = warp & 3;
-    int lt = 0;
+    int lt = 0, nst = 0;
     for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
       const Tile4 ti = decode4(p, g);
       const bool set_ok = tile_set(p, ti.t) >= 0;
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       if (p.pow_acc) {
         epi_power(p, tmem_base, ti, ncb, q, lane, acc, set_ok);
       } else {
-        for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok);
+        for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok, nst);
       }
       if (tid == 256 && lt < 8) K4TR(144 + lt);
       __syncwarp();
@@ -745,7 +755,7 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   p.tma_last = env_last != 0 && st_ok && S_AB * AB_STAGE >= 4 * 8 * EPI_WARP;
   if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
     return cudaErrorInvalidValue;
-  p.s_raw = p.tma_store ? S_RAW_MAX - 1 : S_RAW_MAX;
+  p.s_raw = p.tma_store ? S_RAW_MAX - 1 - K4_EPI_DB : S_RAW_MAX;
   // y loads marked evict_first when every y element is read once and in one wave (tiles <= SMs, disjoint window
   // inputs): measured -1.6% on config 3 (10.66 -> 10.48 us, same box); with overlapping windows or several tiles
   // per SM the re-reads need y in L2 (configs 4-5 lost 8-10% with it).  Evict-first h stores measured no gain.
