@@ -171,7 +171,8 @@ int ce_launch_count(const ce_handle *h, int64_t *out);
  * CE_COMB_FULL (12W): group g outputs the S tones S*g + q (every tone); one weight set per UE.
  * CE_COMB_SUB  (3W):  group g outputs the G tones S*g + s + (S/G) q; weights shared by all UEs; every
  *                     other tone holds the last estimate at or before it (the first estimate before it).
- * Readings C1-C4 in DESIGN.md.
+ * Readings C1-C6 in DESIGN.md (C6: under K10 a non-finite LS value -- a zero pilot symbol -- reaches every output of
+ * the 16-pilot block windows that hold it, not only the groups whose G-pilot windows use it).
  * ------------------------------------------------------------------------------------------------- */
 typedef enum { CE_COMB_FULL = 0, CE_COMB_SUB = 1 } ce_comb_mode;
 
@@ -191,7 +192,8 @@ typedef struct {
  * CE_ENOMEM as ce_init. */
 int ce_comb_init(const ce_comb_params *p, ce_comb_handle **out);
 /* K6a: FP64 Cholesky build of every (UE, type) weight, rounded to complex64; synchronises the stream
- * once to read the positive-definite flag (CE_ENOTPD). */
+ * once to read the positive-definite flag (CE_ENOTPD); for K10-capable shapes also builds K10's bf16 hi / lo weight
+ * images from those weights (one more kernel and stream synchronisation). */
 int ce_comb_build_filters(ce_comb_handle *h, void *stream);
 /* Hot path on device pointers (K10, or K6b: ce_comb_set_kernel), asynchronous on `stream`:
  *   d_y : complex64 [T][M][N]     received pilot OFDM symbol of each antenna (all UEs on their combs)
@@ -209,7 +211,8 @@ int ce_comb_launch_count(const ce_comb_handle *h, int64_t *out);
 /* Estimator kernel of ce_comb_estimate.  AUTO (default): K10 -- the 12W on tcgen05 (BF16x3 products, FP32
  * accumulation; LS de-interleaved per UE by k10_ls, then one GEMM per (UE, block of groups, 128 rows)) -- when
  * mode == CE_COMB_FULL, G <= 13, N even and the call has at least 4 units of work per SM
- * (ceil(T*M / 128) * n_ue * blocks, ~N/(4S) blocks), else K6b (FP32 SIMT; one launch, faster on small calls).  SIMT
+ * (ceil(T*M / 128) * n_ue * blocks; a block is up to floor(64/S) groups whose pilot windows fit one 16-pilot window:
+ * ~N/(4S) blocks for the 12W), else K6b (FP32 SIMT; one launch, faster on small calls).  SIMT
  * forces K6b; TC forces K10 for every call (CE_EINVAL when the shape is not supported).  K10 keeps a per-handle
  * device workspace for the LS planes (2 * n_ue * T*M * ceil4(N/S) * 4 bytes), grown on the first call that needs
  * more (a cudaMalloc outside any stream order, so a handle's calls must not overlap on different streams). */
