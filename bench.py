@@ -783,6 +783,29 @@ def run_comb(args):
                     "d2h_bytes_per_step": int(out_bytes), "steps": e2e_steps},
             "gpu_launches": int(launches), "clocks": clk.summary(), "device": torch.cuda.get_device_name(dev),
         }
+        if world == 1 and not args.no_cpu_baseline:
+            # the oracle on a bounded sample (antenna 0 of every instance), timed on the host cores; the timed buffers'
+            # estimates of that antenna are its parity sample (every y buffer holds the same draw)
+            import oracle
+            times = []
+            t_start = time.perf_counter()
+            while len(times) < 3 or time.perf_counter() - t_start < args.cpu_budget_s / 2:
+                t0 = time.perf_counter()
+                ref = oracle.comb_estimate(y[:, :1], x, r, s2, cfg.N, cfg.S, cfg.G, cfg.mode, cfg.n_ue)
+                times.append(time.perf_counter() - t0)
+            med = float(np.median(times))
+            line["cpu_baseline"] = {"value": T * cfg.n_ue * N / med, "unit": "estimates/s", "cores": _cores(),
+                                    "kind": "oracle", "runs": len(times), "cpu_model": _cpu_model(),
+                                    "blas": _blas_vendor(),
+                                    "sample": f"oracle comb_estimate (complex128) on antenna 0 of all {T} instances; "
+                                              f"median of {len(times)} runs"}
+            hs = h_dev[0][:, :1].cpu().numpy().astype(np.complex128)
+            d = (hs - ref).reshape(T, -1)
+            inst = np.linalg.norm(d, axis=1) / np.linalg.norm(ref.reshape(T, -1), axis=1)
+            rows = np.linalg.norm(hs - ref, axis=-1) / np.maximum(np.linalg.norm(ref, axis=-1), 1e-300)
+            line["parity"] = {"max_rel_err_per_instance": float(inst.max()), "max_row_rel_err": float(rows.max()),
+                              "bar": "1e-4 per instance, 1e-3 per row",
+                              "sample": "the timed buffers' estimates of antenna 0 (all instances, all UEs) vs the oracle"}
         print(json.dumps(line), flush=True)
     est.close()
     dd.close()
@@ -868,6 +891,30 @@ def run_stats(args):
                                                 "BF16 peak / 3 plus the noise-window DFT 8 C N B at the FP32 peak")},
             "gpu_launches": (5 if k9 and k4n else 3) * args.steps, "clocks": clk.summary(),
             "device": torch.cuda.get_device_properties(0).name}
+    if not args.no_cpu_baseline:
+        # the oracle as it stands on a bounded sample (instance 0, antennas [0, m)), timed on the host cores; the same
+        # sample through ce_stats_estimate (outside the timed region) is its parity check
+        import oracle
+        m = max(1, min(cfg.M, 8))
+        ys, xs = y[:1, :m], x[:1]
+        times = []
+        t_start = time.perf_counter()
+        while len(times) < 3 or time.perf_counter() - t_start < args.cpu_budget_s / 2:
+            t0 = time.perf_counter()
+            r_o, s2_o = oracle.estimate_stats(ys, xs, D, B)
+            times.append(time.perf_counter() - t0)
+        rg, s2g = ce.ce_stats_estimate(torch.from_numpy(np.ascontiguousarray(ys)).cuda(),
+                                       torch.from_numpy(np.ascontiguousarray(xs)).cuda(), D, B)
+        torch.cuda.synchronize()
+        rg, s2g = rg.cpu().numpy()[0], float(s2g.cpu().numpy()[0])
+        med = float(np.median(times))
+        line["cpu_baseline"] = {"value": m * cfg.K * cfg.N / med, "unit": "samples/s", "cores": _cores(),
+                                "kind": "oracle", "runs": len(times), "cpu_model": _cpu_model(), "blas": _blas_vendor(),
+                                "sample": f"oracle estimate_stats (complex128) on antennas [0,{m}) of config "
+                                          f"{cfg.cfg_id} instance 0; median of {len(times)} runs"}
+        line["parity"] = {"max_rel_err_r": float(np.max(np.abs(rg - r_o)) / abs(r_o[0])),
+                          "rel_err_sigma2": abs(s2g / s2_o - 1.0), "bar": "1e-4 (tests/test_gpu_stats.py)",
+                          "sample": "ce_stats_estimate on the same sample vs the oracle"}
     print(json.dumps(line), flush=True)
 
 
