@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "ce_internal.h"
@@ -89,6 +90,18 @@ constexpr int K4_SMEM_ST = S_AB * AB_STAGE + (S_RAW_MAX - 1 - K4_EPI_DB) * RAW_S
 constexpr int K4_SMEM_NOST = S_AB * AB_STAGE + S_RAW_MAX * RAW_STAGE + BAR_BYTES + 1024;
 constexpr int K4_SMEM = K4_SMEM_ST > K4_SMEM_NOST ? K4_SMEM_ST : K4_SMEM_NOST;
 static_assert(K4_SMEM <= 232448, "K4 shared memory");
+// Pair mode (k4_bf16x3<true>, a cluster of two CTAs = tcgen05 cta_group::2, M = 256): each CTA keeps its own 128 A
+// rows and HALF of the filter chunk's rows (the pair's MMA reads both halves), so a stage is 32 KB instead of 48 KB
+// and the raw ring gets the difference: 5 stages with the TMA-store staging, 6 without.
+constexpr int S_RAW_BARS = 6;              // raw-ring barrier slots (>= every ring depth used)
+constexpr int B_PLANE_P = B_PLANE / 2;     // 8 KB
+constexpr int AB_STAGE_P = 2 * A_PLANE + 2 * B_PLANE_P;   // 32 KB
+constexpr int S_RAW_P_ST = 5 - K4_EPI_DB, S_RAW_P_NOST = 6;
+constexpr int K4P_SMEM_ST = S_AB * AB_STAGE_P + S_RAW_P_ST * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
+constexpr int K4P_SMEM_NOST = S_AB * AB_STAGE_P + S_RAW_P_NOST * RAW_STAGE + BAR_BYTES + 1024;
+constexpr int K4P_SMEM = K4P_SMEM_ST > K4P_SMEM_NOST ? K4P_SMEM_ST : K4P_SMEM_NOST;
+static_assert(K4P_SMEM <= 232448, "K4 pair shared memory");
+static_assert(S_RAW_MAX <= S_RAW_BARS && S_RAW_P_NOST <= S_RAW_BARS, "raw-ring barrier slots");
 
 struct K4Params {
   float2 *h;
@@ -96,8 +109,9 @@ struct K4Params {
   const uint16_t *bank_lo;
   const Window *geo;         // device window table (read only when n_win > MAXW_PARAM)
   const int32_t *soi;
-  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
+  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;   // n_ct: 128-row column tiles (pair mode: 256-row pair tiles)
   int n_tiles;               // T * n_win * n_ct
+  int pair;                  // 1: k4_bf16x3<true>; CTA rank r of a pair takes the 128-row tile 2 * (g % n_ct) + r
   int tma_store;             // 1: interior 32-float column blocks leave through SW128 staging + TMA stores
   int tma_last;              // 1: the same for each CTA's last tile, staged in the then idle A/B ring
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
@@ -113,10 +127,10 @@ struct Tile4 {
   int t, ct, a, o, kept, n0, off, nw;
 };
 
-__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g) {
+__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank = 0) {
   Tile4 ti;
   // column block fastest (measured faster than window-fastest on configs 3-5)
-  ti.ct = g % p.n_ct;
+  ti.ct = p.pair ? 2 * (g % p.n_ct) + rank : g % p.n_ct;
   const int rest = g / p.n_ct;
   const int w = rest % p.n_win;
   ti.t = rest / p.n_win;
@@ -152,6 +166,13 @@ __device__ __forceinline__ void st_out(float2 *ptr, float2 v) {
 #else
   *ptr = v;
 #endif
+}
+// arrive on the leader's (cluster rank 0) copy of `bar`: local for rank 0, remote for rank 1 (release, cluster scope)
+__device__ __forceinline__ void arrive_leader(uint64_t *bar, int rank) {
+  if (rank == 0)
+    asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  else
+    mbar_arrive_remote(bar, 0);
 }
 __device__ __forceinline__ float rcp_approx(float v) {
   float r;
@@ -275,6 +296,7 @@ __device__ __forceinline__ void epi_power(const K4Params &p, uint32_t tmem_base,
   }
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
               const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K4Params p) {
@@ -282,21 +304,28 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
   // visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int ABS = PAIR ? AB_STAGE_P : AB_STAGE;     // bytes per A/B stage
+  constexpr int BPL = PAIR ? B_PLANE_P : B_PLANE;       // bytes per B plane (pair: this CTA's half of the rows)
   uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
   const int S_RAW = p.s_raw;
-  uint8_t *raw = smem + S_AB * AB_STAGE;                // [S_RAW][y 16 KB | x 4 KB]
+  uint8_t *raw = smem + S_AB * ABS;                     // [S_RAW][y 16 KB | x 4 KB]
   uint8_t *epi = raw + S_RAW * RAW_STAGE;               // [4 warps][EPI_WARP] when p.tma_store
   uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? EPI_BYTES : 0));
-  uint64_t *raw_full = bars;                            // [S_RAW_MAX]
-  uint64_t *raw_empty = bars + S_RAW_MAX;               // [S_RAW_MAX]
-  uint64_t *a_full = bars + 2 * S_RAW_MAX;              // [S_AB]  transform done
+  uint64_t *raw_full = bars;                            // [S_RAW_BARS]
+  uint64_t *raw_empty = bars + S_RAW_BARS;              // [S_RAW_BARS]
+  uint64_t *a_full = bars + 2 * S_RAW_BARS;             // [S_AB]  transform done (pair: the leader's, both CTAs)
   uint64_t *b_full = a_full + S_AB;                     // [S_AB]  filter chunk landed
   uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
   uint64_t *tmem_full = st_empty + S_AB;                // [2]
-  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp (pair: the leader's)
+  uint64_t *b_peer = tmem_empty + 2;                    // [S_AB]  pair: the peer's half of the filter chunk landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_peer + S_AB);
+  static_assert((2 * S_RAW_BARS + 4 * S_AB + 4) * 8 + 4 <= BAR_BYTES, "barrier block");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = PAIR ? int(cluster_ctarank()) : 0;
+  const int g_first = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);   // pair mode: both CTAs walk the pair's tiles
+  const int g_step = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
 #ifdef CE_K4_TRACE
   if (tid == 0 && g_k4_trace) {
     unsigned long long gt;
@@ -306,18 +335,19 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #endif
   if (tid == 0) {
     K4TR(1);
-    for (int s = 0; s < S_RAW_MAX; ++s) {
+    for (int s = 0; s < S_RAW_BARS; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], NTR);
     }
     for (int s = 0; s < S_AB; ++s) {
-      mbar_init(&a_full[s], NTR);
+      mbar_init(&a_full[s], PAIR ? 16 : NTR);          // pair: one arrival per transform warp of both CTAs
       mbar_init(&b_full[s], 1);
       mbar_init(&st_empty[s], 1);
+      mbar_init(&b_peer[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4);
+      mbar_init(&tmem_empty[i], PAIR ? 8 : 4);         // pair: the epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     K4TR(203);
@@ -330,7 +360,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (warp == 12 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
-    if (int(blockIdx.x) < p.n_tiles) ti0 = decode4(p, blockIdx.x);
+    if (g_first < p.n_tiles) ti0 = decode4(p, g_first, rank);
     K0 = p.K;
     cols0 = p.cols;
     nkc0 = p.nkc;
@@ -339,11 +369,15 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     asm volatile("" ::"r"(row0_0), "r"(xbytes0), "r"(nkc0), "r"(ti0.a), "r"(ti0.t), "r"(cols0) : "memory");
   }
   if (warp == 13) {
-    tmem_alloc(tmem_slot, 512);
+    if (PAIR)
+      tmem_alloc2(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
     if (lane == 0) K4TR(202);
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();           // the peer's barriers are initialised before any remote arrive / multicast commit
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tid == 0) {
@@ -367,12 +401,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     if (lane == 0) {
       const uint32_t xbytes = uint32_t(xbytes0);
       int it = 0;
-      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
-        const Tile4 ti = g == int(blockIdx.x) ? ti0 : decode4(p, g);
+      for (int g = g_first; g < p.n_tiles; g += g_step) {
+        const Tile4 ti = g == g_first ? ti0 : decode4(p, g, rank);
 #ifdef CE_K4_TRACE
-        if (g == int(blockIdx.x)) c_dec = clock64();
+        if (g == g_first) c_dec = clock64();
 #endif
-        const int row0 = g == int(blockIdx.x) ? row0_0 : ti.t * cols0 + ti.ct * TM;
+        const int row0 = g == g_first ? row0_0 : ti.t * cols0 + ti.ct * TM;
         for (int kc = 0; kc < nkc0; ++kc, ++it) {
           const int s = it % S_RAW;
           mbar_wait(&raw_empty[s], ((it / S_RAW) & 1) ^ 1);
@@ -409,8 +443,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int jp = tid & 7;            // complex pair 2jp, 2jp+1 of the 16-complex chunk
     const int rb = tid >> 3;           // rows rb + 32 i, i < 4
     int it = 0;
-    for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
-      const Tile4 ti = decode4(p, g);
+    for (int g = g_first; g < p.n_tiles; g += g_step) {
+      const Tile4 ti = decode4(p, g, rank);
       const int c_first = ti.ct * TM + rb;
       const int x_first = c_first % p.K;
       const int x_step = 32 % p.K;
@@ -452,7 +486,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
         mbar_arrive(&raw_empty[sr]);           // the raw slot is consumed (values used above): refill it
         mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
-        uint8_t *ah = ab + sa * AB_STAGE;
+        uint8_t *ah = ab + sa * ABS;
         uint8_t *al = ah + A_PLANE;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -468,7 +502,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
         fence_proxy_async();
         if (tid == 0 && it < 24) K4TR(56 + it);
-        mbar_arrive(&a_full[sa]);
+        if constexpr (PAIR) {
+          __syncwarp();
+          if (lane == 0) arrive_leader(&a_full[sa], rank);
+        } else {
+          mbar_arrive(&a_full[sa]);
+        }
       }
     }
   } else if (warp < 12) {
@@ -477,10 +516,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // -> direct 8-byte stores: each warp instruction writes 8 rows x 32 contiguous bytes.
     const int q = warp & 3;
     int lt = 0, nst = 0;
-    for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
-      const Tile4 ti = decode4(p, g);
+    for (int g = g_first; g < p.n_tiles; g += g_step, ++lt) {
+      const Tile4 ti = decode4(p, g, rank);
       const bool set_ok = tile_set(p, ti.t) >= 0;
-      const bool last = p.tma_last && g + int(gridDim.x) >= p.n_tiles;
+      const bool last = p.tma_last && g + g_step >= p.n_tiles;
       const int acc = lt & 1;
       mbar_wait(&tmem_full[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -495,7 +534,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);
+        if (PAIR)
+          arrive_leader(&tmem_empty[acc], rank);
+        else
+          mbar_arrive(&tmem_empty[acc]);
       }
     }
     if ((p.tma_store || p.tma_last) && lane == 0) bulk_wait0();   // every TMA store of this warp completed
@@ -503,10 +545,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     // ---------------------------------------------------------------- B producer
     if (lane == 0) {
       int it = 0;
-      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x) {
-        const Tile4 ti = decode4(p, g);
+      for (int g = g_first; g < p.n_tiles; g += g_step) {
+        const Tile4 ti = decode4(p, g, rank);
         const int set = p.bank_shared ? 0 : max(tile_set(p, ti.t), 0);
-        const uint32_t bytes = uint32_t(ti.nw) * 64;          // per plane
+        const int nrows = PAIR ? ti.nw >> 1 : ti.nw;          // pair: this CTA's half of the chunk's rows
+        const uint32_t bytes = uint32_t(nrows) * 64;          // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
@@ -516,56 +559,88 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #endif
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
-          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0) * 32;   // bf16 elements
-          uint8_t *bh = ab + s * AB_STAGE + 2 * A_PLANE;
+          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * nrows) * 32;   // bf16 elements
+          uint8_t *bh = ab + s * ABS + 2 * A_PLANE;
           if (p.l2_hint & 8) {
             const uint64_t pol = l2_evict_last_policy();
             bulk_g2s_hint(bh, p.bank_hi + src, bytes, &b_full[s], pol);
-            bulk_g2s_hint(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s], pol);
+            bulk_g2s_hint(bh + BPL, p.bank_lo + src, bytes, &b_full[s], pol);
           } else {
             bulk_g2s(bh, p.bank_hi + src, bytes, &b_full[s]);
-            bulk_g2s(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s]);
+            bulk_g2s(bh + BPL, p.bank_lo + src, bytes, &b_full[s]);
           }
         }
       }
     }
   } else {
     // ---------------------------------------------------------------- MMA issuer (warp 13)
-    if (lane == 0) {
+    if (lane == 0 && PAIR && rank != 0) {
+      // pair mode, peer CTA: the leader issues the pair's MMAs; this thread only tells it when the peer's half of
+      // each filter chunk has landed (bulk copies signal a barrier of their own CTA)
+      int it = 0;
+      for (int g = g_first; g < p.n_tiles; g += g_step) {
+        for (int kc = 0; kc < p.nkc; ++kc, ++it) {
+          const int s = it % S_AB;
+          mbar_wait(&b_full[s], (it / S_AB) & 1);
+          mbar_arrive_remote(&b_peer[s], 0);
+        }
+      }
+    } else if (lane == 0) {
       int it = 0, lt = 0;
-      for (int g = blockIdx.x; g < p.n_tiles; g += gridDim.x, ++lt) {
-        const Tile4 ti = decode4(p, g);
+      for (int g = g_first; g < p.n_tiles; g += g_step, ++lt) {
+        const Tile4 ti = decode4(p, g, rank);
         const int acc = lt & 1;
-        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128
+        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128 (pair: 256 = 128 rows per CTA)
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(ti.nw >> 3) << 17) |
-                               (uint32_t(TM >> 4) << 24);
-        mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+                               (uint32_t((PAIR ? 2 * TM : TM) >> 4) << 24);
+        if (PAIR)
+          mbar_wait_cluster(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+        else
+          mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * NMAXW);
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
           const int s = it % S_AB;
           const uint32_t ph = (it / S_AB) & 1;
-          mbar_wait(&a_full[s], ph);
-          mbar_wait(&b_full[s], ph);
+          if (PAIR) {
+            mbar_wait_cluster(&a_full[s], ph);
+            mbar_wait(&b_full[s], ph);
+            mbar_wait_cluster(&b_peer[s], ph);
+          } else {
+            mbar_wait(&a_full[s], ph);
+            mbar_wait(&b_full[s], ph);
+          }
           tc_fence_after();
           if (it < 24) K4TR(104 + it);
-          uint8_t *st = ab + s * AB_STAGE;
+          uint8_t *st = ab + s * ABS;
           const uint64_t ah = sw64_desc(smem_u32(st));
           const uint64_t al = sw64_desc(smem_u32(st + A_PLANE));
           const uint64_t bh = sw64_desc(smem_u32(st + 2 * A_PLANE));
-          const uint64_t bl = sw64_desc(smem_u32(st + 2 * A_PLANE + B_PLANE));
+          const uint64_t bl = sw64_desc(smem_u32(st + 2 * A_PLANE + BPL));
           const int nks = min(2, nks_total - 2 * kc);
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t adv = uint64_t(2 * ks);      // +32 bytes along K
 #ifndef K4_ABL_NOMMA
-            mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-            mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
-            mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+            if (PAIR) {
+              mma_bf16_pair(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+              mma_bf16_pair(d, ah + adv, bl + adv, idesc, 1u);
+              mma_bf16_pair(d, al + adv, bh + adv, idesc, 1u);
+            } else {
+              mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+              mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
+              mma_bf16(d, al + adv, bh + adv, idesc, 1u);
+            }
 #endif
           }
-          mma_commit(&st_empty[s]);
+          if (PAIR)
+            mma_commit_pair(&st_empty[s]);
+          else
+            mma_commit(&st_empty[s]);
         }
-        mma_commit(&tmem_full[acc]);
+        if (PAIR)
+          mma_commit_pair(&tmem_full[acc]);
+        else
+          mma_commit(&tmem_full[acc]);
         if (lt < 8) K4TR(128 + lt);
         else if (lt < 32) K4TR(152 + lt - 8);
       }
@@ -574,6 +649,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   tc_fence_before();
   if (tid == 256) K4TR(3);
   __syncthreads();
+  if (PAIR) cluster_sync();           // neither CTA leaves while the other may still reach its barriers or TMEM
   if (tid == 0) K4TR(4);
 #ifdef CE_K4_TRACE
   if (tid == 0 && g_k4_trace) {   // end globaltimer: tools/k4_trace.cu calibrates clock64 against it
@@ -585,7 +661,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (warp == 13) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (PAIR)
+      tmem_dealloc2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 
@@ -650,6 +729,7 @@ __global__ void k4_build_dft_bank(int N, int B, int lo, int nkc, int NR, uint16_
 struct DevInfo {
   bool init = false;
   int num_sms = 0;
+  int max_pairs = 0;   // CTA pairs (clusters of 2) of k4_bf16x3<true> resident at once
 };
 cudaError_t dev_info(DevInfo **out) {
   static DevInfo infos[64];
@@ -661,8 +741,32 @@ cudaError_t dev_info(DevInfo **out) {
   if (!d.init) {
     e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k4_bf16x3, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
+    e = cudaFuncSetAttribute(k4_bf16x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k4_bf16x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4P_SMEM);
+    if (e != cudaSuccess) return e;
+    {
+      // a persistent pair grid must not exceed the clusters the device can hold at once (a second wave would
+      // double the time): ask the occupancy calculator rather than assuming num_sms / 2
+      cudaLaunchConfig_t oc = {};
+      oc.gridDim = dim3(unsigned(d.num_sms & ~1));
+      oc.blockDim = dim3(K4_THREADS);
+      oc.dynamicSmemBytes = K4P_SMEM;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = 2;
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      oc.attrs = ca;
+      oc.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, k4_bf16x3<true>, &oc) != cudaSuccess) {
+        (void)cudaGetLastError();
+        nc = 0;
+      }
+      d.max_pairs = nc < d.num_sms / 2 ? nc : d.num_sms / 2;
+      if (getenv("CE_K4_DEBUG")) fprintf(stderr, "k4: %d SMs, %d resident CTA pairs\n", d.num_sms, nc);
+    }
     d.init = true;
   }
   *out = &d;
@@ -738,6 +842,15 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   p.bank_shared = a.bank_shared ? 1 : 0;
   p.cols = a.M * a.K;
   p.n_ct = (p.cols + TM - 1) / TM;
+  // Pair mode (cta_group::2): two CTAs of a cluster share each filter chunk.  CE_K4_PAIR = 0 / 1 forces it off / on
+  // (experiments); the default policy is below.
+  static const int env_pair = getenv("CE_K4_PAIR") ? atoi(getenv("CE_K4_PAIR")) : -1;
+  static const int env_pairs = getenv("CE_K4_PAIRS") ? atoi(getenv("CE_K4_PAIRS")) : 0;   // experiments: grid pairs
+  const int max_pairs = env_pairs > 0 && env_pairs < di->max_pairs ? env_pairs : di->max_pairs;
+  const bool pair = (env_pair >= 0 ? env_pair != 0 : false) && max_pairs >= 1 && p.n_ct >= 2;
+  p.pair = pair ? 1 : 0;
+  if (pair) p.n_ct = (p.n_ct + 1) / 2;
+  const int n_units = pair ? max_pairs : di->num_sms;   // CTAs, or CTA pairs, resident at once
   for (int w = 0; w < MAXW_PARAM; ++w) p.geo_s[w] = w < a.n_win && a.geo_host ? a.geo_host[w] : Window{0, 0, 0};
   const long long tiles = (long long)a.T * a.n_win * p.n_ct;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -750,12 +863,17 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   // -11% on config 5); a one-tile-per-SM launch (config 3) keeps the 4-deep raw ring and direct stores.
   static const int env_st = getenv("CE_K4_TMA_STORE") ? atoi(getenv("CE_K4_TMA_STORE")) : -1;   // experiments
   const bool st_ok = (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0 && a.pow_acc == nullptr;
-  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) && st_ok;
+  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)n_units) && st_ok;
   static const int env_last = getenv("CE_K4_TMA_LAST") ? atoi(getenv("CE_K4_TMA_LAST")) : 1;   // experiments
-  p.tma_last = env_last != 0 && st_ok && S_AB * AB_STAGE >= 4 * 8 * EPI_WARP;
+  if (pair)
+    p.s_raw = p.tma_store ? S_RAW_P_ST : S_RAW_P_NOST;
+  else
+    p.s_raw = p.tma_store ? S_RAW_MAX - 1 - K4_EPI_DB : S_RAW_MAX;
+  // a CTA's last tile stages its 4 x 8 output blocks in the then idle A/B ring (pair mode: and the raw ring behind it)
+  p.tma_last = env_last != 0 && st_ok &&
+               (pair ? S_AB * AB_STAGE_P + p.s_raw * RAW_STAGE : S_AB * AB_STAGE) >= 4 * 8 * EPI_WARP;
   if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
     return cudaErrorInvalidValue;
-  p.s_raw = p.tma_store ? S_RAW_MAX - 1 - K4_EPI_DB : S_RAW_MAX;
   // y loads marked evict_first when every y element is read once and in one wave (tiles <= SMs, disjoint window
   // inputs): measured -1.6% on config 3 (10.66 -> 10.48 us, same box); with overlapping windows or several tiles
   // per SM the re-reads need y in L2 (configs 4-5 lost 8-10% with it).  Evict-first h stores measured no gain.
@@ -764,14 +882,25 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   static const int env_hint = getenv("CE_K4_L2HINT") ? atoi(getenv("CE_K4_L2HINT")) : -1;   // experiments
   // pilots and filter-bank chunks (re-read by every column tile) evict_last: config 3 -0.5%, config 4 -0.8% (same
   // box, two repetitions), configs 5-6 equal
-  p.l2_hint = env_hint >= 0 ? env_hint : ((tiles <= (long long)di->num_sms && disjoint ? 1 : 0) | 4 | 8);
+  p.l2_hint = env_hint >= 0 ? env_hint : ((tiles <= (long long)n_units && disjoint ? 1 : 0) | 4 | 8);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
+  const unsigned units = unsigned(tiles < n_units ? tiles : n_units);
+  cfg.gridDim = dim3(pair ? 2 * units : units);
   cfg.blockDim = dim3(K4_THREADS);
-  cfg.dynamicSmemBytes = p.tma_store ? K4_SMEM_ST : K4_SMEM_NOST;
+  if (pair)
+    cfg.dynamicSmemBytes = p.tma_store ? K4P_SMEM_ST : K4P_SMEM_NOST;
+  else
+    cfg.dynamicSmemBytes = p.tma_store ? K4_SMEM_ST : K4_SMEM_NOST;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   int na = 0;
+  if (pair) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
 #ifndef K4_NO_PDL
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[na].val.programmaticStreamSerializationAllowed = 1;
@@ -779,7 +908,8 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
 #endif
   cfg.attrs = at;
   cfg.numAttrs = na;
-  e = cudaLaunchKernelEx(&cfg, k4_bf16x3, tmy, tmx, tmh, p);
+  e = pair ? cudaLaunchKernelEx(&cfg, k4_bf16x3<true>, tmy, tmx, tmh, p)
+           : cudaLaunchKernelEx(&cfg, k4_bf16x3<false>, tmy, tmx, tmh, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }
