@@ -76,7 +76,7 @@ constexpr int EPI_WARP = 4096;             // TMA-store staging per epilogue war
 #endif
 constexpr int EPI_NB = K4_EPI_DB ? 2 : 1;
 constexpr int EPI_BYTES = 4 * EPI_NB * EPI_WARP;
-constexpr int BAR_BYTES = 256;
+constexpr int BAR_BYTES = 320;
 constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
 
 #ifndef K4_S_AB
@@ -96,9 +96,22 @@ static_assert(K4_SMEM <= 232448, "K4 shared memory");
 constexpr int S_RAW_BARS = 6;              // raw-ring barrier slots (>= every ring depth used)
 constexpr int B_PLANE_P = B_PLANE / 2;     // 8 KB
 constexpr int AB_STAGE_P = 2 * A_PLANE + 2 * B_PLANE_P;   // 32 KB
-constexpr int S_RAW_P_ST = 5 - K4_EPI_DB, S_RAW_P_NOST = 6;
-constexpr int K4P_SMEM_ST = S_AB * AB_STAGE_P + S_RAW_P_ST * RAW_STAGE + EPI_BYTES + BAR_BYTES + 1024;
-constexpr int K4P_SMEM_NOST = S_AB * AB_STAGE_P + S_RAW_P_NOST * RAW_STAGE + BAR_BYTES + 1024;
+#ifndef K4_S_AB_P
+#define K4_S_AB_P 4          // measured: config 5 1419-1440 us with 4 stages (and 4 raw), 1450-1474 with 3 (and 5 raw); config 4 equal
+#endif
+#ifndef K4_EPI_DB_P
+#define K4_EPI_DB_P 0        // experiments: 1 = two staging boxes per epilogue warp in pair mode
+#endif
+constexpr int S_AB_P = K4_S_AB_P;          // A/B stages in pair mode
+constexpr int EPI_NB_P = K4_EPI_DB_P ? 2 : 1;
+constexpr int EPI_BYTES_P = 4 * EPI_NB_P * EPI_WARP;
+// raw stages: whatever the 227 KB leave (at most S_RAW_BARS)
+constexpr int raw_fit(int rest) { return rest / RAW_STAGE > 6 ? 6 : rest / RAW_STAGE; }
+constexpr int S_RAW_P_ST = raw_fit(232448 - 1024 - BAR_BYTES - S_AB_P * AB_STAGE_P - EPI_BYTES_P);
+constexpr int S_RAW_P_NOST = raw_fit(232448 - 1024 - BAR_BYTES - S_AB_P * AB_STAGE_P);
+constexpr int K4P_SMEM_ST = S_AB_P * AB_STAGE_P + S_RAW_P_ST * RAW_STAGE + EPI_BYTES_P + BAR_BYTES + 1024;
+constexpr int K4P_SMEM_NOST = S_AB_P * AB_STAGE_P + S_RAW_P_NOST * RAW_STAGE + BAR_BYTES + 1024;
+static_assert(S_RAW_P_ST >= 2 && S_AB_P <= 4, "K4 pair ring depths");
 constexpr int K4P_SMEM = K4P_SMEM_ST > K4P_SMEM_NOST ? K4P_SMEM_ST : K4P_SMEM_NOST;
 static_assert(K4P_SMEM <= 232448, "K4 pair shared memory");
 static_assert(S_RAW_MAX <= S_RAW_BARS && S_RAW_P_NOST <= S_RAW_BARS, "raw-ring barrier slots");
@@ -167,12 +180,25 @@ __device__ __forceinline__ void st_out(float2 *ptr, float2 v) {
   *ptr = v;
 #endif
 }
-// arrive on the leader's (cluster rank 0) copy of `bar`: local for rank 0, remote for rank 1 (release, cluster scope)
+// arrive on the leader's (cluster rank 0) copy of `bar`: local for rank 0, remote for rank 1
 __device__ __forceinline__ void arrive_leader(uint64_t *bar, int rank) {
-  if (rank == 0)
+  if (rank == 0) {
+#ifdef CE_PAIR_REL_CLUSTER
     asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-  else
+#else
+    mbar_arrive(bar);
+#endif
+  } else {
     mbar_arrive_remote(bar, 0);
+  }
+}
+// the leader's waits on barriers the peer arrives on
+__device__ __forceinline__ void wait_pair(uint64_t *bar, uint32_t parity) {
+#ifdef CE_PAIR_REL_CLUSTER
+  mbar_wait_cluster(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 __device__ __forceinline__ float rcp_approx(float v) {
   float r;
@@ -185,6 +211,7 @@ __device__ __forceinline__ float rcp_approx(float v) {
 // the instance) leave through SW128 staging and one TMA store of [32 rows][128 B] (full-line writes issued
 // by the TMA engine); the rest use direct 8-byte stores (8 rows x 32 B per warp instruction).  On a CTA's
 // last tile the A/B ring is idle and every (warp, block) gets its own staging buffer there.
+template <int NB>
 __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *tmh, uint32_t tmem_base, uint8_t *ab,
                                           uint8_t *epi, const Tile4 &ti, int cb, int q, int lane, int acc, bool last,
                                           bool set_ok, int &nst) {
@@ -198,9 +225,9 @@ __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *
   tmem_ld_wait();
   if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
       ti.ct * TM + q * 32 + 32 <= p.cols) {
-    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + (q * EPI_NB + (nst % EPI_NB)) * EPI_WARP;
+    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + (q * NB + (nst % NB)) * EPI_WARP;
     if (!last && lane == 0) {                        // the store that used this staging buffer has read it
-      if (EPI_NB == 2)
+      if (NB == 2)
         bulk_wait_read1();
       else
         bulk_wait_read0();
@@ -304,23 +331,24 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
   // visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int SAB = PAIR ? S_AB_P : S_AB;             // A/B stages
   constexpr int ABS = PAIR ? AB_STAGE_P : AB_STAGE;     // bytes per A/B stage
   constexpr int BPL = PAIR ? B_PLANE_P : B_PLANE;       // bytes per B plane (pair: this CTA's half of the rows)
-  uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
+  uint8_t *ab = smem;                                   // [SAB][A_hi | A_lo | B_hi | B_lo]
   const int S_RAW = p.s_raw;
-  uint8_t *raw = smem + S_AB * ABS;                     // [S_RAW][y 16 KB | x 4 KB]
+  uint8_t *raw = smem + SAB * ABS;                     // [S_RAW][y 16 KB | x 4 KB]
   uint8_t *epi = raw + S_RAW * RAW_STAGE;               // [4 warps][EPI_WARP] when p.tma_store
-  uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? EPI_BYTES : 0));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? (PAIR ? EPI_BYTES_P : EPI_BYTES) : 0));
   uint64_t *raw_full = bars;                            // [S_RAW_BARS]
   uint64_t *raw_empty = bars + S_RAW_BARS;              // [S_RAW_BARS]
-  uint64_t *a_full = bars + 2 * S_RAW_BARS;             // [S_AB]  transform done (pair: the leader's, both CTAs)
-  uint64_t *b_full = a_full + S_AB;                     // [S_AB]  filter chunk landed
-  uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
-  uint64_t *tmem_full = st_empty + S_AB;                // [2]
+  uint64_t *a_full = bars + 2 * S_RAW_BARS;             // [SAB]  transform done (pair: the leader's, both CTAs)
+  uint64_t *b_full = a_full + SAB;                     // [SAB]  filter chunk landed
+  uint64_t *st_empty = b_full + SAB;                   // [SAB]  MMAs reading the stage done (commit)
+  uint64_t *tmem_full = st_empty + SAB;                // [2]
   uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp (pair: the leader's)
-  uint64_t *b_peer = tmem_empty + 2;                    // [S_AB]  pair: the peer's half of the filter chunk landed
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_peer + S_AB);
-  static_assert((2 * S_RAW_BARS + 4 * S_AB + 4) * 8 + 4 <= BAR_BYTES, "barrier block");
+  uint64_t *b_peer = tmem_empty + 2;                    // [SAB]  pair: the peer's half of the filter chunk landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_peer + SAB);
+  static_assert((2 * S_RAW_BARS + 4 * SAB + 4) * 8 + 4 <= BAR_BYTES, "barrier block");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = PAIR ? int(cluster_ctarank()) : 0;
@@ -339,7 +367,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], NTR);
     }
-    for (int s = 0; s < S_AB; ++s) {
+    for (int s = 0; s < SAB; ++s) {
       mbar_init(&a_full[s], PAIR ? 16 : NTR);          // pair: one arrival per transform warp of both CTAs
       mbar_init(&b_full[s], 1);
       mbar_init(&st_empty[s], 1);
@@ -449,12 +477,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       const int x_first = c_first % p.K;
       const int x_step = 32 % p.K;
       for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-        const int sr = it % S_RAW, sa = it % S_AB;
+        const int sr = it % S_RAW, sa = it % SAB;
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
         if (tid == 0 && it < 24) K4TR(32 + it);
 #ifdef K4_ABL_NOTRANSFORM
         mbar_arrive(&raw_empty[sr]);
-        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
+        mbar_wait(&st_empty[sa], ((it / SAB) & 1) ^ 1);
         mbar_arrive(&a_full[sa]);
         continue;
 #endif
@@ -485,7 +513,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           lv[i][1] = pack_bf16(l1r - bf16_lo_f(hv[i][1]), l1i - bf16_hi_f(hv[i][1]));
         }
         mbar_arrive(&raw_empty[sr]);           // the raw slot is consumed (values used above): refill it
-        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
+        mbar_wait(&st_empty[sa], ((it / SAB) & 1) ^ 1);
         uint8_t *ah = ab + sa * ABS;
         uint8_t *al = ah + A_PLANE;
 #pragma unroll
@@ -528,7 +556,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       if (p.pow_acc) {
         epi_power(p, tmem_base, ti, ncb, q, lane, acc, set_ok);
       } else {
-        for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok, nst);
+        for (int cb = 0; cb < ncb; ++cb) epi_block<(PAIR ? EPI_NB_P : EPI_NB)>(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok, nst);
       }
       if (tid == 256 && lt < 8) K4TR(144 + lt);
       __syncwarp();
@@ -551,8 +579,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         const int nrows = PAIR ? ti.nw >> 1 : ti.nw;          // pair: this CTA's half of the chunk's rows
         const uint32_t bytes = uint32_t(nrows) * 64;          // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % S_AB;
-          mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
+          const int s = it % SAB;
+          mbar_wait(&st_empty[s], ((it / SAB) & 1) ^ 1);
 #ifdef K4_ABL_NOB
           mbar_arrive(&b_full[s]);
           continue;
@@ -580,8 +608,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       int it = 0;
       for (int g = g_first; g < p.n_tiles; g += g_step) {
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % S_AB;
-          mbar_wait(&b_full[s], (it / S_AB) & 1);
+          const int s = it % SAB;
+          mbar_wait(&b_full[s], (it / SAB) & 1);
           mbar_arrive_remote(&b_peer[s], 0);
         }
       }
@@ -594,18 +622,20 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(ti.nw >> 3) << 17) |
                                (uint32_t((PAIR ? 2 * TM : TM) >> 4) << 24);
         if (PAIR)
-          mbar_wait_cluster(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+          wait_pair(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         else
           mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * NMAXW);
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % S_AB;
-          const uint32_t ph = (it / S_AB) & 1;
+          const int s = it % SAB;
+          const uint32_t ph = (it / SAB) & 1;
           if (PAIR) {
-            mbar_wait_cluster(&a_full[s], ph);
+            wait_pair(&a_full[s], ph);
             mbar_wait(&b_full[s], ph);
-            mbar_wait_cluster(&b_peer[s], ph);
+#ifndef K4_ABL_NOPEER
+            wait_pair(&b_peer[s], ph);
+#endif
           } else {
             mbar_wait(&a_full[s], ph);
             mbar_wait(&b_full[s], ph);
@@ -847,7 +877,12 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
   static const int env_pair = getenv("CE_K4_PAIR") ? atoi(getenv("CE_K4_PAIR")) : -1;
   static const int env_pairs = getenv("CE_K4_PAIRS") ? atoi(getenv("CE_K4_PAIRS")) : 0;   // experiments: grid pairs
   const int max_pairs = env_pairs > 0 && env_pairs < di->max_pairs ? env_pairs : di->max_pairs;
-  const bool pair = (env_pair >= 0 ? env_pair != 0 : false) && max_pairs >= 1 && p.n_ct >= 2;
+  // Policy: pairs when every CTA walks more than two tiles (configs 4-5: -2 % / -4..6 % same box); a launch of one
+  // tile per SM (config 3) is 11 % slower in pairs (the cluster barrier in the prologue, chunk-level lockstep of the
+  // two CTAs), and the power mode keeps single CTAs (not measured in pairs).
+  const long long tiles128 = (long long)a.T * a.n_win * p.n_ct;
+  const bool pair = (env_pair >= 0 ? env_pair != 0 : (tiles128 > 2LL * di->num_sms && a.pow_acc == nullptr)) &&
+                    max_pairs >= 1 && p.n_ct >= 2;
   p.pair = pair ? 1 : 0;
   if (pair) p.n_ct = (p.n_ct + 1) / 2;
   const int n_units = pair ? max_pairs : di->num_sms;   // CTAs, or CTA pairs, resident at once
@@ -871,7 +906,7 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
     p.s_raw = p.tma_store ? S_RAW_MAX - 1 - K4_EPI_DB : S_RAW_MAX;
   // a CTA's last tile stages its 4 x 8 output blocks in the then idle A/B ring (pair mode: and the raw ring behind it)
   p.tma_last = env_last != 0 && st_ok &&
-               (pair ? S_AB * AB_STAGE_P + p.s_raw * RAW_STAGE : S_AB * AB_STAGE) >= 4 * 8 * EPI_WARP;
+               (pair ? S_AB_P * AB_STAGE_P + p.s_raw * RAW_STAGE : S_AB * AB_STAGE) >= 4 * 8 * EPI_WARP;
   if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
     return cudaErrorInvalidValue;
   // y loads marked evict_first when every y element is read once and in one wave (tiles <= SMs, disjoint window

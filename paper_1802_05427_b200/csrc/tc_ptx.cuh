@@ -223,11 +223,19 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-// arrive (release, cluster scope) on the mbarrier at `bar`'s offset in CTA `rank` of the cluster
+// arrive on the mbarrier at `bar`'s offset in CTA `rank` of the cluster.  Default semantics (release at CTA scope),
+// as for a local arrive: the data the barrier guards stays in the arriving CTA's own shared memory (the pair's MMA
+// reads each CTA's operands in place), so only the signal crosses CTAs.  A release at CLUSTER scope here cost 1-2 us
+// per arrive in K4's pair mode (trace: the arrive returned only after the SM's outstanding loads had drained), which
+// made the pair 1.7x slower than two single CTAs; -DCE_PAIR_REL_CLUSTER restores it for the A/B.
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+#ifdef CE_PAIR_REL_CLUSTER
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+#endif
 }
 __device__ __forceinline__ void tmem_alloc2(uint32_t *slot, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
