@@ -68,6 +68,11 @@ cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets,
                                    uint16_t *bank_lo, cudaStream_t stream, int64_t *launches);
 cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
                                    cudaStream_t stream, int64_t *launches);
+// K4 on CTA pairs (k4p_block_lmmse_pair.cu: tcgen05 cta_group::2, each CTA of a cluster holds half of the filter
+// chunk); bf16x3_pair_wanted is the policy launch_contract_bf16x3 consults (CE_K4_PAIR = 0 / 1 overrides it).
+bool bf16x3_pair_wanted(const ContractArgs &a);
+cudaError_t launch_contract_bf16x3_pair(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
+                                        cudaStream_t stream, int64_t *launches);
 // K4's bank for the unitary N-point inverse DFT at the B delay bins lo .. lo + B - 1 (rows = bins, K = tones): one
 // set, nkc = ceil(2N / 32) chunks of NR = ceil(2B / 16) * 16 rows, bf16 hi / lo planes.
 void dft_bank_shape(int32_t N, int32_t B, int32_t *nkc, int32_t *NR);

@@ -1,5 +1,5 @@
-"""Run by tests/test_gpu_parity.py::test_k4_store_paths in a subprocess (CE_K4_TMA_STORE is read once per
-process): K4 (CE_KERNEL_BF16X3) against the oracle on shapes that mix the epilogue's TMA-store column blocks
+"""Run by tests/test_gpu_parity.py::test_k4_store_paths and ::test_k4_pair_paths in a subprocess (CE_K4_TMA_STORE
+and CE_K4_PAIR are read once per process): K4 (CE_KERNEL_BF16X3) against the oracle on shapes that mix the epilogue's TMA-store column blocks
 (interior, 16-byte aligned, full 32-row warp groups) with its direct-store blocks (window edges, odd output
 starts, ragged column tiles, tails).  Exit status 0 = every instance within 1e-4."""
 import sys
@@ -16,6 +16,7 @@ SHAPES = [  # N, b, s, M, K, T
     (300, 50, 24, 16, 16, 3),       # overlapping windows: off = 2, odd output starts
     (130, 64, 64, 5, 7, 2),         # 35 columns: no warp group is complete -> direct stores only
     (512, 96, 64, 32, 8, 2),        # 256 columns = two full tiles, clamped last window
+    (1200, 100, 100, 32, 12, 2),    # 384 columns = three tiles: in pair mode the last pair's second CTA has no tile
 ]
 
 

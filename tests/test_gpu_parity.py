@@ -341,3 +341,20 @@ def test_k4_store_paths(tma_store):
     res = subprocess.run([sys.executable, os.path.join(root, "tests", "_k4_store_paths.py")], env=env,
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+@pytest.mark.parametrize("tma_store", ["1", "0"])
+def test_k4_pair_paths(tma_store):
+    """K4's pair variant (k4_bf16x3_pair: two CTAs of a cluster on one tcgen05 cta_group::2 MMA, half of each filter
+    chunk per CTA) forced on for every launch with at least two column tiles (CE_K4_PAIR=1; AUTO takes it only for
+    config-5-like launches), with both store paths, on the shapes of tests/_k4_store_paths.py -- ragged second
+    tiles, an odd number of column tiles (a pair whose second CTA has no tile), overlapping windows, a bad set
+    index.  Same operation and bar as K4: Eq. 12 per block, 1e-4 per instance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CE_K4_PAIR="1", CE_K4_TMA_STORE=tma_store, PYTHONPATH=root)
+    res = subprocess.run([sys.executable, os.path.join(root, "tests", "_k4_store_paths.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr

@@ -6,6 +6,9 @@ mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build_${TAG}.log 2>&1 || { echo BUILD FAILED; tail -20 gpurun_out/build_${TAG}.log; exit 1; }
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest gpu exit $?"; tail -2 gpurun_out/pytest_gpu_${TAG}.log
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_${TAG}.log 2>&1; echo "smoke exit $?"
+# K4 pair mode (cta_group::2) forced on every K4 shape with >= 2 column tiles: the same parity / guard-band tests
+CE_K4_PAIR=1 timeout 900 python -m pytest tests/test_gpu_tc_paths.py tests/test_gpu_parity.py tests/test_gpu_guard.py -q -m gpu \
+  -k "not stats and not comb" > gpurun_out/pytest_gpu_pair_${TAG}.log 2>&1; echo "pytest gpu (pair forced) exit $?"; tail -2 gpurun_out/pytest_gpu_pair_${TAG}.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_${TAG}_driverlike.json 2> gpurun_out/bench_${TAG}_driverlike.err; echo "bench20 exit $?"
 timeout 900 python bench.py --steps 2000 --warmup 50 --sweep-steps 40 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench2000 exit $?"
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; echo "ref exit $?"

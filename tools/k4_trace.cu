@@ -12,6 +12,7 @@
 #include "../include/ce.h"
 
 extern "C" int ce_k4_trace_set(void *dptr);
+extern "C" int ce_k4p_trace_set(void *dptr);   // the pair variant (k4p_block_lmmse_pair.cu) keeps its own trace pointer
 
 int main(int argc, char **argv) {
   int N = argc > 1 ? atoi(argv[1]) : 1200, b = argc > 2 ? atoi(argv[2]) : 100, s = argc > 3 ? atoi(argv[3]) : 100;
@@ -61,7 +62,7 @@ int main(int argc, char **argv) {
   ce_selected_kernel(h, &sel);
   printf("kernel %d: %.2f us per call (untraced, back-to-back)\n", sel, 1e3 * ms / reps);
   ce_k4_trace_set(dtr);
-  ce_k4_trace_set(dtr);
+  ce_k4p_trace_set(dtr);
   for (int i = 0; i < 3; ++i) {
     ce_estimate(h, dy[i % NB], dx, dh[i % NB], T, M, K, nullptr, nullptr);
     cudaDeviceSynchronize();
