@@ -1,9 +1,8 @@
-// K4 pair variant (k4_bf16x3_pair) -- K4's fused LS + block-LMMSE contraction (k4_block_lmmse_bf16x3.cu: tcgen05
-// kind::f16 on BF16 operands, error-compensated "BF16x3": D = A_hi B_hi + A_hi B_lo + A_lo B_hi, FP32 accumulation in
-// TMEM; reading B1) on CTA PAIRS: tcgen05 cta_group::2, M = 256.  The pipeline, roles and epilogue are
-// K4's (the description below is K4's own); what the pair changes is in the "Pair mode" paragraph at its end.  The
-// file is K4's source with PAIR fixed to true: the single-CTA kernel keeps a translation unit of its own because the
-// same source compiled for both (a template over PAIR) ran config 3 9 % slower than K4 (9.89 -> 10.81 us, same box).
+// K4 -- fused LS + block-LMMSE contraction on tcgen05 (kind::f16, BF16 operands), error-compensated
+// "BF16x3":  D = A_hi B_hi + A_hi B_lo + A_lo B_hi,  X_hi = bf16_rn(X), X_lo = bf16_rn(X - X_hi),
+// FP32 accumulation in TMEM.  Per-product error <= ~3 * 2^-18 (the dropped A_lo B_lo term and the
+// rounding of the lo parts); reading B1 derives the bound (measured ~1e-6 relative Frobenius
+// error on configs 2-5 against the 1e-4 bar).
 //
 // Same operation as K2/K3 (Eq. 12 per block, LS of Eq. 9 fused into the load) and
 // the same complex -> real embedding as K3 (A = interleaved LS row, D = interleaved output row,
@@ -30,23 +29,10 @@
 // The window table rides in the kernel parameters (no dependent global load before the first TMA), and
 // the kernel is launched with programmatic stream serialization (PDL): its launch overlaps the previous
 // kernel's tail; griddepcontrol.wait precedes every access to caller data.
-//
-// Pair mode (k4_bf16x3_pair; launches bf16x3_pair_wanted() selects -- config-5-like): a cluster of two CTAs on one TPC works
-// on two adjacent 128-row tiles of the same (instance, window) as ONE tcgen05 cta_group::2 MMA of M = 256.  Each
-// CTA transforms its own rows into its own A stage and fetches HALF of the filter chunk's rows (the pair's MMA
-// reads both halves in place), so the filter-bank stream per SM and the B bytes each MMA reads from shared memory
-// halve; A and B keep rings of their own (3 A stages of 16 KB, 5 B stages of 16 KB, 4 raw stages).  The leader (rank 0)
-// issues every MMA; its a_full / tmem_empty barriers count the warps of both CTAs (one arrive per warp, the peer's
-// through mapa + mbarrier.arrive on the leader's barrier), the peer's MMA warp forwards "my half of the chunk has
-// landed" (bulk copies can only signal a barrier of their own CTA), and the commits are multicast to both CTAs.
-// The cross-CTA arrives keep the default CTA-scope release: the data they guard stays in the arriving CTA's own
-// shared memory, and a CLUSTER-scope release cost 1-2 us per arrive (the arrive returned only after the SM's
-// outstanding loads had drained -- the pair ran 1.7x slower than two single CTAs with it).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <cstdio>
 #include <cstdlib>
 
 #include "ce_internal.h"
@@ -72,7 +58,6 @@ __device__ unsigned long long *g_k4_trace;
   } while (0)
 #endif
 
-constexpr bool PAIR = true;                // this file is K4's pair variant; K4 proper is k4_block_lmmse_bf16x3.cu
 constexpr int K4_THREADS = 480;            // 15 warps: 8 transform, 4 epilogue, 3 single-thread roles
 constexpr int NTR = 256;                   // transform threads
 constexpr int CK = 16;                     // complex per K chunk = 32 bf16 = 64-byte rows
@@ -90,7 +75,7 @@ constexpr int EPI_WARP = 4096;             // TMA-store staging per epilogue war
 #endif
 constexpr int EPI_NB = K4_EPI_DB ? 2 : 1;
 constexpr int EPI_BYTES = 4 * EPI_NB * EPI_WARP;
-constexpr int BAR_BYTES = 384;
+constexpr int BAR_BYTES = 256;
 constexpr int MAXW_PARAM = 32;             // windows carried in the kernel parameters
 
 #ifndef K4_S_AB
@@ -104,40 +89,6 @@ constexpr int K4_SMEM_ST = S_AB * AB_STAGE + (S_RAW_MAX - 1 - K4_EPI_DB) * RAW_S
 constexpr int K4_SMEM_NOST = S_AB * AB_STAGE + S_RAW_MAX * RAW_STAGE + BAR_BYTES + 1024;
 constexpr int K4_SMEM = K4_SMEM_ST > K4_SMEM_NOST ? K4_SMEM_ST : K4_SMEM_NOST;
 static_assert(K4_SMEM <= 232448, "K4 shared memory");
-// Pair mode (a cluster of two CTAs = tcgen05 cta_group::2, M = 256): each CTA keeps its own 128 A rows and HALF of
-// the filter chunk's rows (the pair's MMA reads both halves); the raw ring gets what the 227 KB leave.
-constexpr int S_RAW_BARS = 6;              // raw-ring barrier slots (>= every ring depth used)
-constexpr int B_PLANE_P = B_PLANE / 2;     // 8 KB
-// pair mode keeps the filter chunks in a ring of their own, deeper than the A ring: a chunk does not depend on
-// the data, so its copy can be issued S_B_P chunks ahead (its L2 latency, ~1 us, otherwise has to hide behind the
-// MMAs of S_AB - 1 chunks)
-constexpr int A_STAGE_P = 2 * A_PLANE;     // 16 KB: A_hi | A_lo
-constexpr int B_STAGE_P = 2 * B_PLANE_P;   // 16 KB: this CTA's half of B_hi | B_lo
-#ifndef K4_S_AB_P
-#define K4_S_AB_P 3          // A stages in pair mode
-#endif
-#ifndef K4_S_B_P
-#define K4_S_B_P 5           // filter-chunk stages in pair mode
-#endif
-#ifndef K4_EPI_DB_P
-#define K4_EPI_DB_P 0        // experiments: 1 = two staging boxes per epilogue warp in pair mode
-#endif
-constexpr int S_AB_P = K4_S_AB_P;          // A stages in pair mode
-constexpr int S_B_P = K4_S_B_P;            // B stages in pair mode
-constexpr int S_B_MAX = 6;                 // B barrier slots
-constexpr int AB_BYTES_P = S_AB_P * A_STAGE_P + S_B_P * B_STAGE_P;
-constexpr int EPI_NB_P = K4_EPI_DB_P ? 2 : 1;
-constexpr int EPI_BYTES_P = 4 * EPI_NB_P * EPI_WARP;
-// raw stages: whatever the 227 KB leave (at most S_RAW_BARS)
-constexpr int raw_fit(int rest) { return rest / RAW_STAGE > 6 ? 6 : rest / RAW_STAGE; }
-constexpr int S_RAW_P_ST = raw_fit(232448 - 1024 - BAR_BYTES - AB_BYTES_P - EPI_BYTES_P);
-constexpr int S_RAW_P_NOST = raw_fit(232448 - 1024 - BAR_BYTES - AB_BYTES_P);
-constexpr int K4P_SMEM_ST = AB_BYTES_P + S_RAW_P_ST * RAW_STAGE + EPI_BYTES_P + BAR_BYTES + 1024;
-constexpr int K4P_SMEM_NOST = AB_BYTES_P + S_RAW_P_NOST * RAW_STAGE + BAR_BYTES + 1024;
-static_assert(S_RAW_P_ST >= 2 && S_AB_P <= 4 && S_B_P <= S_B_MAX && S_AB <= S_B_MAX, "K4 pair ring depths");
-constexpr int K4P_SMEM = K4P_SMEM_ST > K4P_SMEM_NOST ? K4P_SMEM_ST : K4P_SMEM_NOST;
-static_assert(K4P_SMEM <= 232448, "K4 pair shared memory");
-static_assert(S_RAW_MAX <= S_RAW_BARS && S_RAW_P_NOST <= S_RAW_BARS, "raw-ring barrier slots");
 
 struct K4Params {
   float2 *h;
@@ -145,9 +96,8 @@ struct K4Params {
   const uint16_t *bank_lo;
   const Window *geo;         // device window table (read only when n_win > MAXW_PARAM)
   const int32_t *soi;
-  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;   // n_ct: 128-row column tiles (pair mode: 256-row pair tiles)
+  int T, K, N, b, n_win, n_sets, nkc, NR, cols, n_ct;
   int n_tiles;               // T * n_win * n_ct
-  int pair;                  // 1: k4_bf16x3_pair; CTA rank r of a pair takes the 128-row tile 2 * (g % n_ct) + r
   int tma_store;             // 1: interior 32-float column blocks leave through SW128 staging + TMA stores
   int tma_last;              // 1: the same for each CTA's last tile, staged in the then idle A/B ring
   int s_raw;                 // raw ring depth (3 with staging, 4 without)
@@ -163,10 +113,10 @@ struct Tile4 {
   int t, ct, a, o, kept, n0, off, nw;
 };
 
-__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank = 0) {
+__device__ __forceinline__ Tile4 decode4(const K4Params &p, int g) {
   Tile4 ti;
   // column block fastest (measured faster than window-fastest on configs 3-5)
-  ti.ct = p.pair ? 2 * (g % p.n_ct) + rank : g % p.n_ct;
+  ti.ct = g % p.n_ct;
   const int rest = g / p.n_ct;
   const int w = rest % p.n_win;
   ti.t = rest / p.n_win;
@@ -203,26 +153,6 @@ __device__ __forceinline__ void st_out(float2 *ptr, float2 v) {
   *ptr = v;
 #endif
 }
-// arrive on the leader's (cluster rank 0) copy of `bar`: local for rank 0, remote for rank 1
-__device__ __forceinline__ void arrive_leader(uint64_t *bar, int rank) {
-  if (rank == 0) {
-#ifdef CE_PAIR_REL_CLUSTER
-    asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-#else
-    mbar_arrive(bar);
-#endif
-  } else {
-    mbar_arrive_remote(bar, 0);
-  }
-}
-// the leader's waits on barriers the peer arrives on
-__device__ __forceinline__ void wait_pair(uint64_t *bar, uint32_t parity) {
-#ifdef CE_PAIR_REL_CLUSTER
-  mbar_wait_cluster(bar, parity);
-#else
-  mbar_wait(bar, parity);
-#endif
-}
 __device__ __forceinline__ float rcp_approx(float v) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -234,7 +164,6 @@ __device__ __forceinline__ float rcp_approx(float v) {
 // the instance) leave through SW128 staging and one TMA store of [32 rows][128 B] (full-line writes issued
 // by the TMA engine); the rest use direct 8-byte stores (8 rows x 32 B per warp instruction).  On a CTA's
 // last tile the A/B ring is idle and every (warp, block) gets its own staging buffer there.
-template <int NB>
 __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *tmh, uint32_t tmem_base, uint8_t *ab,
                                           uint8_t *epi, const Tile4 &ti, int cb, int q, int lane, int acc, bool last,
                                           bool set_ok, int &nst) {
@@ -248,9 +177,9 @@ __device__ __forceinline__ void epi_block(const K4Params &p, const CUtensorMap *
   tmem_ld_wait();
   if ((p.tma_store || last) && 32 * cb >= ti.off && 32 * cb + 32 <= ti.off + nf && ((2 * ti.o - ti.off) & 3) == 0 &&
       ti.ct * TM + q * 32 + 32 <= p.cols) {
-    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + (q * NB + (nst % NB)) * EPI_WARP;
+    uint8_t *stg = last ? ab + (q * 8 + cb) * EPI_WARP : epi + (q * EPI_NB + (nst % EPI_NB)) * EPI_WARP;
     if (!last && lane == 0) {                        // the store that used this staging buffer has read it
-      if (NB == 2)
+      if (EPI_NB == 2)
         bulk_wait_read1();
       else
         bulk_wait_read0();
@@ -347,44 +276,28 @@ __device__ __forceinline__ void epi_power(const K4Params &p, uint32_t tmem_base,
 }
 
 __global__ void __launch_bounds__(K4_THREADS, 1)
-    k4_bf16x3_pair(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
+    k4_bf16x3(const __grid_constant__ CUtensorMap tmy, const __grid_constant__ CUtensorMap tmx,
               const __grid_constant__ CUtensorMap tmh, const __grid_constant__ K4Params p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (keeps the shared address space
   // visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int SAB = PAIR ? S_AB_P : S_AB;             // A stages
-  constexpr int SB = PAIR ? S_B_P : S_AB;               // B stages (without pairs: the same ring as A)
-  constexpr int BPL = PAIR ? B_PLANE_P : B_PLANE;       // bytes per B plane (pair: this CTA's half of the rows)
-  // single CTAs: [S_AB][A_hi | A_lo | B_hi | B_lo]; pairs: [SAB][A_hi | A_lo] then [SB][B_hi | B_lo]
-  constexpr int A_STRIDE = PAIR ? A_STAGE_P : AB_STAGE, B_STRIDE = PAIR ? B_STAGE_P : AB_STAGE;
-  constexpr int B_BASE = PAIR ? S_AB_P * A_STAGE_P : 2 * A_PLANE;
-  constexpr int AB_BYTES = PAIR ? AB_BYTES_P : S_AB * AB_STAGE;
-  uint8_t *ab = smem;
+  uint8_t *ab = smem;                                   // [S_AB][A_hi | A_lo | B_hi | B_lo]
   const int S_RAW = p.s_raw;
-  uint8_t *raw = smem + AB_BYTES;                       // [S_RAW][y 16 KB | x 4 KB]
+  uint8_t *raw = smem + S_AB * AB_STAGE;                // [S_RAW][y 16 KB | x 4 KB]
   uint8_t *epi = raw + S_RAW * RAW_STAGE;               // [4 warps][EPI_WARP] when p.tma_store
-  uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? (PAIR ? EPI_BYTES_P : EPI_BYTES) : 0));
-  uint64_t *raw_full = bars;                            // [S_RAW_BARS]
-  uint64_t *raw_empty = bars + S_RAW_BARS;              // [S_RAW_BARS]
-  uint64_t *a_full = bars + 2 * S_RAW_BARS;             // [SAB]  transform done (pair: the leader's, both CTAs)
-  uint64_t *st_empty = a_full + 4;                      // [SAB]  MMAs reading the A stage done (commit)
-  uint64_t *b_full = st_empty + 4;                      // [SB]   filter chunk landed
-  uint64_t *b_empty_p = b_full + S_B_MAX;               // [SB]   pair: MMAs reading the B stage done (commit)
-  uint64_t *b_empty = PAIR ? b_empty_p : st_empty;      //        single CTAs: one ring, one barrier
-  uint64_t *tmem_full = b_empty_p + S_B_MAX;            // [2]
-  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp (pair: the leader's)
-  uint64_t *b_peer = tmem_empty + 2;                    // [SB]   pair: the peer's half of the filter chunk landed
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_peer + S_B_MAX);
-  static_assert((2 * S_RAW_BARS + 8 + 3 * S_B_MAX + 4) * 8 + 4 <= BAR_BYTES && SAB <= 4, "barrier block");
+  uint64_t *bars = reinterpret_cast<uint64_t *>(epi + (p.tma_store ? EPI_BYTES : 0));
+  uint64_t *raw_full = bars;                            // [S_RAW_MAX]
+  uint64_t *raw_empty = bars + S_RAW_MAX;               // [S_RAW_MAX]
+  uint64_t *a_full = bars + 2 * S_RAW_MAX;              // [S_AB]  transform done
+  uint64_t *b_full = a_full + S_AB;                     // [S_AB]  filter chunk landed
+  uint64_t *st_empty = b_full + S_AB;                   // [S_AB]  MMAs reading the stage done (commit)
+  uint64_t *tmem_full = st_empty + S_AB;                // [2]
+  uint64_t *tmem_empty = tmem_full + 2;                 // [2]     one arrival per epilogue warp
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // both CTAs of a pair walk the pair's tiles.  Re-read from the special / constant registers at every use, as K4
-  // does: holding them in registers from the top of the kernel cost K4 0.7 us per launch and 2.5 % on config 4
-  // (bisected, tools/ab_bisect.sh)
-#define g_first int(blockIdx.x >> 1)
-#define rank int(blockIdx.x & 1)   /* = %cluster_ctarank for clusters of two along x */
-#define g_step int(gridDim.x >> 1)
+  const int g_first = int(blockIdx.x), g_step = int(gridDim.x);
 #ifdef CE_K4_TRACE
   if (tid == 0 && g_k4_trace) {
     unsigned long long gt;
@@ -394,22 +307,18 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #endif
   if (tid == 0) {
     K4TR(1);
-    for (int s = 0; s < S_RAW_BARS; ++s) {
+    for (int s = 0; s < S_RAW_MAX; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], NTR);
     }
-    for (int s = 0; s < SAB; ++s) {
-      mbar_init(&a_full[s], PAIR ? 16 : NTR);          // pair: one arrival per transform warp of both CTAs
-      mbar_init(&st_empty[s], 1);
-    }
-    for (int s = 0; s < SB; ++s) {
+    for (int s = 0; s < S_AB; ++s) {
+      mbar_init(&a_full[s], NTR);
       mbar_init(&b_full[s], 1);
-      mbar_init(&b_peer[s], 1);
-      if (PAIR) mbar_init(&b_empty_p[s], 1);
+      mbar_init(&st_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], PAIR ? 8 : 4);         // pair: the epilogue warps of both CTAs
+      mbar_init(&tmem_empty[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     K4TR(203);
@@ -422,7 +331,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (warp == 12 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
-    if (g_first < p.n_tiles) ti0 = decode4(p, g_first, rank);
+    if (g_first < p.n_tiles) ti0 = decode4(p, g_first);
     K0 = p.K;
     cols0 = p.cols;
     nkc0 = p.nkc;
@@ -431,15 +340,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     asm volatile("" ::"r"(row0_0), "r"(xbytes0), "r"(nkc0), "r"(ti0.a), "r"(ti0.t), "r"(cols0) : "memory");
   }
   if (warp == 13) {
-    if (PAIR)
-      tmem_alloc2(tmem_slot, 512);
-    else
-      tmem_alloc(tmem_slot, 512);
+    tmem_alloc(tmem_slot, 512);
     if (lane == 0) K4TR(202);
   }
   tc_fence_before();
   __syncthreads();
-  if (PAIR) cluster_sync();           // the peer's barriers are initialised before any remote arrive / multicast commit
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tid == 0) {
@@ -464,7 +369,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       const uint32_t xbytes = uint32_t(xbytes0);
       int it = 0;
       for (int g = g_first; g < p.n_tiles; g += g_step) {
-        const Tile4 ti = g == g_first ? ti0 : decode4(p, g, rank);
+        const Tile4 ti = g == g_first ? ti0 : decode4(p, g);
 #ifdef CE_K4_TRACE
         if (g == g_first) c_dec = clock64();
 #endif
@@ -506,17 +411,17 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int rb = tid >> 3;           // rows rb + 32 i, i < 4
     int it = 0;
     for (int g = g_first; g < p.n_tiles; g += g_step) {
-      const Tile4 ti = decode4(p, g, rank);
+      const Tile4 ti = decode4(p, g);
       const int c_first = ti.ct * TM + rb;
       const int x_first = c_first % p.K;
       const int x_step = 32 % p.K;
       for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-        const int sr = it % S_RAW, sa = it % SAB;
+        const int sr = it % S_RAW, sa = it % S_AB;
         mbar_wait(&raw_full[sr], (it / S_RAW) & 1);
         if (tid == 0 && it < 24) K4TR(32 + it);
 #ifdef K4_ABL_NOTRANSFORM
         mbar_arrive(&raw_empty[sr]);
-        mbar_wait(&st_empty[sa], ((it / SAB) & 1) ^ 1);
+        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
         mbar_arrive(&a_full[sa]);
         continue;
 #endif
@@ -547,8 +452,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           lv[i][1] = pack_bf16(l1r - bf16_lo_f(hv[i][1]), l1i - bf16_hi_f(hv[i][1]));
         }
         mbar_arrive(&raw_empty[sr]);           // the raw slot is consumed (values used above): refill it
-        mbar_wait(&st_empty[sa], ((it / SAB) & 1) ^ 1);
-        uint8_t *ah = ab + sa * A_STRIDE;
+        mbar_wait(&st_empty[sa], ((it / S_AB) & 1) ^ 1);
+        uint8_t *ah = ab + sa * AB_STAGE;
         uint8_t *al = ah + A_PLANE;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -564,12 +469,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
         fence_proxy_async();
         if (tid == 0 && it < 24) K4TR(56 + it);
-        if (PAIR) {
-          __syncwarp();
-          if (lane == 0) arrive_leader(&a_full[sa], rank);
-        } else {
-          mbar_arrive(&a_full[sa]);
-        }
+        mbar_arrive(&a_full[sa]);
       }
     }
   } else if (warp < 12) {
@@ -579,7 +479,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const int q = warp & 3;
     int lt = 0, nst = 0;
     for (int g = g_first; g < p.n_tiles; g += g_step, ++lt) {
-      const Tile4 ti = decode4(p, g, rank);
+      const Tile4 ti = decode4(p, g);
       const bool set_ok = tile_set(p, ti.t) >= 0;
       const bool last = p.tma_last && g + g_step >= p.n_tiles;
       const int acc = lt & 1;
@@ -590,16 +490,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       if (p.pow_acc) {
         epi_power(p, tmem_base, ti, ncb, q, lane, acc, set_ok);
       } else {
-        for (int cb = 0; cb < ncb; ++cb) epi_block<(PAIR ? EPI_NB_P : EPI_NB)>(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok, nst);
+        for (int cb = 0; cb < ncb; ++cb) epi_block(p, &tmh, tmem_base, ab, epi, ti, cb, q, lane, acc, last, set_ok, nst);
       }
       if (tid == 256 && lt < 8) K4TR(144 + lt);
       __syncwarp();
       if (lane == 0) {
         tc_fence_before();
-        if (PAIR)
-          arrive_leader(&tmem_empty[acc], rank);
-        else
-          mbar_arrive(&tmem_empty[acc]);
+        mbar_arrive(&tmem_empty[acc]);
       }
     }
     if ((p.tma_store || p.tma_last) && lane == 0) bulk_wait0();   // every TMA store of this warp completed
@@ -608,105 +505,68 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int g = g_first; g < p.n_tiles; g += g_step) {
-        const Tile4 ti = decode4(p, g, rank);
+        const Tile4 ti = decode4(p, g);
         const int set = p.bank_shared ? 0 : max(tile_set(p, ti.t), 0);
-        const int nrows = PAIR ? ti.nw >> 1 : ti.nw;          // pair: this CTA's half of the chunk's rows
-        const uint32_t bytes = uint32_t(nrows) * 64;          // per plane
+        const uint32_t bytes = uint32_t(ti.nw) * 64;          // per plane
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % SB;
-          mbar_wait(&b_empty[s], ((it / SB) & 1) ^ 1);
+          const int s = it % S_AB;
+          mbar_wait(&st_empty[s], ((it / S_AB) & 1) ^ 1);
 #ifdef K4_ABL_NOB
           mbar_arrive(&b_full[s]);
           continue;
 #endif
           mbar_arrive_expect_tx(&b_full[s], 2 * bytes);
           if (it < 24) K4TR(80 + it);
-          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0 + rank * nrows) * 32;   // bf16 elements
-          uint8_t *bh = ab + B_BASE + s * B_STRIDE;
+          const size_t src = ((size_t(set) * p.nkc + kc) * p.NR + ti.n0) * 32;   // bf16 elements
+          uint8_t *bh = ab + s * AB_STAGE + 2 * A_PLANE;
           if (p.l2_hint & 8) {
             const uint64_t pol = l2_evict_last_policy();
             bulk_g2s_hint(bh, p.bank_hi + src, bytes, &b_full[s], pol);
-            bulk_g2s_hint(bh + BPL, p.bank_lo + src, bytes, &b_full[s], pol);
+            bulk_g2s_hint(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s], pol);
           } else {
             bulk_g2s(bh, p.bank_hi + src, bytes, &b_full[s]);
-            bulk_g2s(bh + BPL, p.bank_lo + src, bytes, &b_full[s]);
+            bulk_g2s(bh + B_PLANE, p.bank_lo + src, bytes, &b_full[s]);
           }
         }
       }
     }
   } else {
     // ---------------------------------------------------------------- MMA issuer (warp 13)
-    if (lane == 0 && PAIR && rank != 0) {
-      // pair mode, peer CTA: the leader issues the pair's MMAs; this thread only tells it when the peer's half of
-      // each filter chunk has landed (bulk copies signal a barrier of their own CTA)
-      int it = 0;
-      for (int g = g_first; g < p.n_tiles; g += g_step) {
-        for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % SB;
-          mbar_wait(&b_full[s], (it / SB) & 1);
-          mbar_arrive_remote(&b_peer[s], 0);
-        }
-      }
-    } else if (lane == 0) {
+    if (lane == 0) {
       int it = 0, lt = 0;
       for (int g = g_first; g < p.n_tiles; g += g_step, ++lt) {
-        const Tile4 ti = decode4(p, g, rank);
+        const Tile4 ti = decode4(p, g);
         const int acc = lt & 1;
-        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128 (pair: 256 = 128 rows per CTA)
+        // F32 accumulate, BF16 A/B, K-major A/B, N = nw, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(ti.nw >> 3) << 17) |
-                               (uint32_t((PAIR ? 2 * TM : TM) >> 4) << 24);
-        if (PAIR)
-          wait_pair(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
-        else
-          mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
+                               (uint32_t(TM >> 4) << 24);
+        mbar_wait(&tmem_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * NMAXW);
         for (int kc = 0; kc < p.nkc; ++kc, ++it) {
-          const int s = it % SAB, sb = it % SB;
-          const uint32_t ph = (it / SAB) & 1, phb = (it / SB) & 1;
-          if (PAIR) {
-            wait_pair(&a_full[s], ph);
-            mbar_wait(&b_full[sb], phb);
-#ifndef K4_ABL_NOPEER
-            wait_pair(&b_peer[sb], phb);
-#endif
-          } else {
-            mbar_wait(&a_full[s], ph);
-            mbar_wait(&b_full[sb], phb);
-          }
+          const int s = it % S_AB;
+          const uint32_t ph = (it / S_AB) & 1;
+          mbar_wait(&a_full[s], ph);
+          mbar_wait(&b_full[s], ph);
           tc_fence_after();
           if (it < 24) K4TR(104 + it);
-          uint8_t *sta = ab + s * A_STRIDE, *stb = ab + B_BASE + sb * B_STRIDE;
-          const uint64_t ah = sw64_desc(smem_u32(sta));
-          const uint64_t al = sw64_desc(smem_u32(sta + A_PLANE));
-          const uint64_t bh = sw64_desc(smem_u32(stb));
-          const uint64_t bl = sw64_desc(smem_u32(stb + BPL));
+          uint8_t *st = ab + s * AB_STAGE;
+          const uint64_t ah = sw64_desc(smem_u32(st));
+          const uint64_t al = sw64_desc(smem_u32(st + A_PLANE));
+          const uint64_t bh = sw64_desc(smem_u32(st + 2 * A_PLANE));
+          const uint64_t bl = sw64_desc(smem_u32(st + 2 * A_PLANE + B_PLANE));
           const int nks = min(2, nks_total - 2 * kc);
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t adv = uint64_t(2 * ks);      // +32 bytes along K
 #ifndef K4_ABL_NOMMA
-            if (PAIR) {
-              mma_bf16_pair(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-              mma_bf16_pair(d, ah + adv, bl + adv, idesc, 1u);
-              mma_bf16_pair(d, al + adv, bh + adv, idesc, 1u);
-            } else {
-              mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
-              mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
-              mma_bf16(d, al + adv, bh + adv, idesc, 1u);
-            }
+            mma_bf16(d, ah + adv, bh + adv, idesc, (kc | ks) != 0);
+            mma_bf16(d, ah + adv, bl + adv, idesc, 1u);
+            mma_bf16(d, al + adv, bh + adv, idesc, 1u);
 #endif
           }
-          if (PAIR) {
-            mma_commit_pair(&st_empty[s]);
-            mma_commit_pair(&b_empty_p[sb]);
-          } else {
-            mma_commit(&st_empty[s]);
-          }
+          mma_commit(&st_empty[s]);
         }
-        if (PAIR)
-          mma_commit_pair(&tmem_full[acc]);
-        else
-          mma_commit(&tmem_full[acc]);
+        mma_commit(&tmem_full[acc]);
         if (lt < 8) K4TR(128 + lt);
         else if (lt < 32) K4TR(152 + lt - 8);
       }
@@ -715,7 +575,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   tc_fence_before();
   if (tid == 256) K4TR(3);
   __syncthreads();
-  if (PAIR) cluster_sync();           // neither CTA leaves while the other may still reach its barriers or TMEM
   if (tid == 0) K4TR(4);
 #ifdef CE_K4_TRACE
   if (tid == 0 && g_k4_trace) {   // end globaltimer: tools/k4_trace.cu calibrates clock64 against it
@@ -727,21 +586,71 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   if (warp == 13) {
     __syncwarp();
     tc_fence_after();
-    if (PAIR)
-      tmem_dealloc2(tmem_base, 512);
-    else
-      tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, 512);
   }
 }
-#undef g_first
-#undef rank
-#undef g_step
 
-// Per-device launch facts: smem attribute set once, SM count, resident CTA pairs.
+// bank[set][kc][n][32] bf16 hi/lo planes of B_r^T[n][32 kc + kk] in the SW64 shared-memory image:
+// row n at n*64 bytes, 16-byte chunk (kk/8) ^ ((n>>1)&3).
+__global__ void k4_build_bank(const float2 *__restrict__ W, int b, int nkc, int NR, uint16_t *__restrict__ bank_hi,
+                              uint16_t *__restrict__ bank_lo) {
+  const int set = blockIdx.x, kc = blockIdx.y;
+  const float2 *Ws = W + size_t(set) * b * b;
+  uint16_t *bh = bank_hi + (size_t(set) * nkc + kc) * NR * 32;
+  uint16_t *bl = bank_lo + (size_t(set) * nkc + kc) * NR * 32;
+  for (int e = threadIdx.x; e < NR * 32; e += blockDim.x) {
+    const int n = e / 32, kk = e % 32;
+    const int k = kc * 32 + kk;
+    const int i = n >> 1, jw = k >> 1;
+    float v = 0.f;
+    if (i < b && jw < b) {
+      const float2 w = Ws[size_t(i) * b + jw];
+      const int sel = ((n & 1) << 1) | (k & 1);
+      v = sel == 0 ? w.x : sel == 1 ? -w.y : sel == 2 ? w.y : w.x;
+    }
+    const uint32_t hi2 = pack_bf16(v, 0.f);          // low half = bf16(v)
+    const float hi = bf16_lo_f(hi2);
+    const uint32_t lo2 = pack_bf16(v - hi, 0.f);
+    const int dst = n * 32 + ((((kk >> 3) ^ ((n >> 1) & 3))) << 3) + (kk & 7);
+    bh[dst] = uint16_t(hi2 & 0xFFFFu);
+    bl[dst] = uint16_t(lo2 & 0xFFFFu);
+  }
+}
+
+// bank[kc][n][32] of the unitary inverse DFT rows W[i][j] = e^{+2 pi i j (lo + i) / N} / sqrt(N), i < B, j < N
+// (zero beyond), same embedding and SW64 image as k4_build_bank; the angle reduced exactly in integers, FP64 sincospi.
+__global__ void k4_build_dft_bank(int N, int B, int lo, int nkc, int NR, uint16_t *__restrict__ bank_hi,
+                                  uint16_t *__restrict__ bank_lo) {
+  const int kc = blockIdx.x;
+  uint16_t *bh = bank_hi + size_t(kc) * NR * 32;
+  uint16_t *bl = bank_lo + size_t(kc) * NR * 32;
+  const double inv_sqrt_n = 1.0 / sqrt(double(N));
+  for (int e = threadIdx.x; e < NR * 32; e += blockDim.x) {
+    const int n = e / 32, kk = e % 32;
+    const int k = kc * 32 + kk;
+    const int i = n >> 1, jw = k >> 1;
+    float v = 0.f;
+    if (i < B && jw < N) {
+      const long long m = (static_cast<long long>(jw) * (lo + i)) % N;
+      double sv, cv;
+      sincospi(2.0 * double(m) / double(N), &sv, &cv);
+      const float2 w = make_float2(float(cv * inv_sqrt_n), float(sv * inv_sqrt_n));
+      const int sel = ((n & 1) << 1) | (k & 1);
+      v = sel == 0 ? w.x : sel == 1 ? -w.y : sel == 2 ? w.y : w.x;
+    }
+    const uint32_t hi2 = pack_bf16(v, 0.f);
+    const float hi = bf16_lo_f(hi2);
+    const uint32_t lo2 = pack_bf16(v - hi, 0.f);
+    const int dst = n * 32 + ((((kk >> 3) ^ ((n >> 1) & 3))) << 3) + (kk & 7);
+    bh[dst] = uint16_t(hi2 & 0xFFFFu);
+    bl[dst] = uint16_t(lo2 & 0xFFFFu);
+  }
+}
+
+// Per-device launch facts: smem attribute set once, SM count.
 struct DevInfo {
   bool init = false;
   int num_sms = 0;
-  int max_pairs = 0;   // CTA pairs (clusters of 2) of k4_bf16x3_pair resident at once
 };
 cudaError_t dev_info(DevInfo **out) {
   static DevInfo infos[64];
@@ -753,28 +662,8 @@ cudaError_t dev_info(DevInfo **out) {
   if (!d.init) {
     e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k4_bf16x3_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, K4P_SMEM);
+    e = cudaFuncSetAttribute(k4_bf16x3, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_SMEM);
     if (e != cudaSuccess) return e;
-    // a persistent pair grid must not exceed the clusters the device can hold at once (a second wave would double
-    // the time): ask the occupancy calculator rather than assuming num_sms / 2
-    cudaLaunchConfig_t oc = {};
-    oc.gridDim = dim3(unsigned(d.num_sms & ~1));
-    oc.blockDim = dim3(K4_THREADS);
-    oc.dynamicSmemBytes = K4P_SMEM;
-    cudaLaunchAttribute ca[1];
-    ca[0].id = cudaLaunchAttributeClusterDimension;
-    ca[0].val.clusterDim.x = 2;
-    ca[0].val.clusterDim.y = 1;
-    ca[0].val.clusterDim.z = 1;
-    oc.attrs = ca;
-    oc.numAttrs = 1;
-    int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, k4_bf16x3_pair, &oc) != cudaSuccess) {
-      (void)cudaGetLastError();
-      nc = 0;
-    }
-    d.max_pairs = nc < d.num_sms / 2 ? nc : d.num_sms / 2;
-    if (getenv("CE_K4_DEBUG")) fprintf(stderr, "k4 pair: %d SMs, %d resident CTA pairs\n", d.num_sms, nc);
     d.init = true;
   }
   *out = &d;
@@ -784,36 +673,53 @@ cudaError_t dev_info(DevInfo **out) {
 }  // namespace
 
 #ifdef CE_K4_TRACE
-extern "C" int ce_k4p_trace_set(void *dptr) {
+extern "C" int ce_k4_trace_set(void *dptr) {
   return int(cudaMemcpyToSymbol(g_k4_trace, &dptr, sizeof(dptr)));
 }
 #endif
 
-// Policy.  CE_K4_PAIR = 0 / 1 forces pairs off / on (experiments).  Default: pairs when every CTA walks more than two
-// 128-row tiles.  Measured, same box, against K4 (two repetitions each): config 5 1486-1488 -> 1400-1435 us
-// (-3.5..6 %), config 4 325-330 -> 314-323 us (-1..5 %); config 3 (one tile per SM) 9.9 -> 11.6 us (the cluster
-// barrier in the prologue, chunk lockstep of the two CTAs).  The power mode keeps single CTAs (not measured in pairs).
-bool bf16x3_pair_wanted(const ContractArgs &a) {
-  static const int env_pair = getenv("CE_K4_PAIR") ? atoi(getenv("CE_K4_PAIR")) : -1;
-  if (env_pair == 0) return false;
-  const int n_ct = (a.M * a.K + TM - 1) / TM;
-  if (n_ct < 2) return false;
-  DevInfo *di = nullptr;
-  if (dev_info(&di) != cudaSuccess || di->max_pairs < 1) return false;
-  if (env_pair > 0) return true;
-  return (long long)a.T * a.n_win * n_ct > 2LL * di->num_sms && a.pow_acc == nullptr;
+void bf16x3_bank_shape(int32_t b, int32_t *nkc, int32_t *NR) {
+  *nkc = (2 * b + 31) / 32;
+  *NR = ((2 * b + 16) + 7) & ~7;
 }
 
-cudaError_t launch_contract_bf16x3_pair(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
-                                        cudaStream_t stream, int64_t *launches) {
+void dft_bank_shape(int32_t N, int32_t B, int32_t *nkc, int32_t *NR) {
+  *nkc = (2 * N + 31) / 32;
+  *NR = (2 * B + 15) & ~15;
+}
+
+cudaError_t launch_build_dft_bank(int32_t N, int32_t B, int32_t lo, uint16_t *bank_hi, uint16_t *bank_lo,
+                                  cudaStream_t stream) {
+  int32_t nkc, NR;
+  dft_bank_shape(N, B, &nkc, &NR);
+  k4_build_dft_bank<<<nkc, 256, 0, stream>>>(N, B, lo, nkc, NR, bank_hi, bank_lo);
+  return cudaGetLastError();
+}
+
+bool bf16x3_launchable(const ContractArgs &a) {
+  const long long rows = (long long)a.T * a.M * a.K;
+  // TMA box starts must be 16-byte aligned: even window starts, even N (row pitch), aligned bases.
+  return a.even_starts && a.K <= KMAX && (a.N % 2) == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && rows < (1LL << 31) && encode_fn() != nullptr;
+}
+
+cudaError_t launch_build_bank_bf16(const float2 *d_W, int32_t b, int32_t n_sets, uint16_t *bank_hi,
+                                   uint16_t *bank_lo, cudaStream_t stream, int64_t *launches) {
+  int32_t nkc, NR;
+  bf16x3_bank_shape(b, &nkc, &NR);
+  k4_build_bank<<<dim3(n_sets, nkc), 256, 0, stream>>>(d_W, b, nkc, NR, bank_hi, bank_lo);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_hi, const uint16_t *bank_lo,
+                                   cudaStream_t stream, int64_t *launches) {
   if (!bf16x3_launchable(a)) return cudaErrorNotSupported;
   if (a.n_win <= MAXW_PARAM && a.geo_host == nullptr) return cudaErrorInvalidValue;
   DevInfo *di = nullptr;
   cudaError_t e = dev_info(&di);
   if (e != cudaSuccess) return e;
-  static const int env_pairs = getenv("CE_K4_PAIRS") ? atoi(getenv("CE_K4_PAIRS")) : 0;   // experiments: grid pairs
-  const int max_pairs = env_pairs > 0 && env_pairs < di->max_pairs ? env_pairs : di->max_pairs;
-  if (max_pairs < 1) return cudaErrorNotSupported;
   K4Params p;
   p.h = a.h;
   p.bank_hi = bank_hi;
@@ -832,8 +738,7 @@ cudaError_t launch_contract_bf16x3_pair(const ContractArgs &a, const uint16_t *b
   p.pow_stride = a.pow_stride;
   p.bank_shared = a.bank_shared ? 1 : 0;
   p.cols = a.M * a.K;
-  p.pair = 1;
-  p.n_ct = ((p.cols + TM - 1) / TM + 1) / 2;          // 256-row pair tiles
+  p.n_ct = (p.cols + TM - 1) / TM;
   for (int w = 0; w < MAXW_PARAM; ++w) p.geo_s[w] = w < a.n_win && a.geo_host ? a.geo_host[w] : Window{0, 0, 0};
   const long long tiles = (long long)a.T * a.n_win * p.n_ct;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -842,33 +747,32 @@ cudaError_t launch_contract_bf16x3_pair(const ContractArgs &a, const uint16_t *b
   if (!cached_map(&tmy, a.y, a.N, (long long)a.T * p.cols, TM) ||
       !cached_map(&tmx, a.x, a.N, (long long)a.T * a.K, a.K))
     return cudaErrorInvalidValue;
-  // same launch rules as K4 (k4_block_lmmse_bf16x3.cu), counted in pairs
+  // TMA stores pay off when CTAs walk several tiles (their stores overlap the next tiles' loads; measured
+  // -11% on config 5); a one-tile-per-SM launch (config 3) keeps the 4-deep raw ring and direct stores.
   static const int env_st = getenv("CE_K4_TMA_STORE") ? atoi(getenv("CE_K4_TMA_STORE")) : -1;   // experiments
   const bool st_ok = (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 && (a.N % 2) == 0 && a.pow_acc == nullptr;
-  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)max_pairs) && st_ok;
+  p.tma_store = (env_st >= 0 ? env_st != 0 : tiles > (long long)di->num_sms) && st_ok;
   static const int env_last = getenv("CE_K4_TMA_LAST") ? atoi(getenv("CE_K4_TMA_LAST")) : 1;   // experiments
-  p.s_raw = p.tma_store ? S_RAW_P_ST : S_RAW_P_NOST;
-  // a CTA's last tile stages its 4 x 8 output blocks in the then idle A and B rings and the raw ring behind them
-  p.tma_last = env_last != 0 && st_ok && AB_BYTES_P + p.s_raw * RAW_STAGE >= 4 * 8 * EPI_WARP;
+  p.tma_last = env_last != 0 && st_ok && S_AB * AB_STAGE >= 4 * 8 * EPI_WARP;
   if ((p.tma_store || p.tma_last) && !cached_map(&tmh, a.h, a.N, (long long)a.T * p.cols, 32, true))
     return cudaErrorInvalidValue;
+  p.s_raw = p.tma_store ? S_RAW_MAX - 1 - K4_EPI_DB : S_RAW_MAX;
+  // y loads marked evict_first when every y element is read once and in one wave (tiles <= SMs, disjoint window
+  // inputs): measured -1.6% on config 3 (10.66 -> 10.48 us, same box); with overlapping windows or several tiles
+  // per SM the re-reads need y in L2 (configs 4-5 lost 8-10% with it).  Evict-first h stores measured no gain.
   bool disjoint = a.geo_host != nullptr;
   for (int w = 0; disjoint && w + 1 < a.n_win; ++w) disjoint = a.geo_host[w + 1].a >= a.geo_host[w].a + a.b;
   static const int env_hint = getenv("CE_K4_L2HINT") ? atoi(getenv("CE_K4_L2HINT")) : -1;   // experiments
-  p.l2_hint = env_hint >= 0 ? env_hint : ((tiles <= (long long)max_pairs && disjoint ? 1 : 0) | 4 | 8);
+  // pilots and filter-bank chunks (re-read by every column tile) evict_last: config 3 -0.5%, config 4 -0.8% (same
+  // box, two repetitions), configs 5-6 equal
+  p.l2_hint = env_hint >= 0 ? env_hint : ((tiles <= (long long)di->num_sms && disjoint ? 1 : 0) | 4 | 8);
   cudaLaunchConfig_t cfg = {};
-  const unsigned units = unsigned(tiles < max_pairs ? tiles : max_pairs);
-  cfg.gridDim = dim3(2 * units);
+  cfg.gridDim = dim3(unsigned(tiles < di->num_sms ? tiles : di->num_sms));
   cfg.blockDim = dim3(K4_THREADS);
-  cfg.dynamicSmemBytes = p.tma_store ? K4P_SMEM_ST : K4P_SMEM_NOST;
+  cfg.dynamicSmemBytes = p.tma_store ? K4_SMEM_ST : K4_SMEM_NOST;
   cfg.stream = stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   int na = 0;
-  at[na].id = cudaLaunchAttributeClusterDimension;
-  at[na].val.clusterDim.x = 2;
-  at[na].val.clusterDim.y = 1;
-  at[na].val.clusterDim.z = 1;
-  ++na;
 #ifndef K4_NO_PDL
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[na].val.programmaticStreamSerializationAllowed = 1;
@@ -876,7 +780,7 @@ cudaError_t launch_contract_bf16x3_pair(const ContractArgs &a, const uint16_t *b
 #endif
   cfg.attrs = at;
   cfg.numAttrs = na;
-  e = cudaLaunchKernelEx(&cfg, k4_bf16x3_pair, tmy, tmx, tmh, p);
+  e = cudaLaunchKernelEx(&cfg, k4_bf16x3, tmy, tmx, tmh, p);
   if (e == cudaSuccess) ++*launches;
   return e;
 }
