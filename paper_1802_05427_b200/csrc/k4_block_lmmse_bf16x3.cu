@@ -718,7 +718,11 @@ cudaError_t launch_contract_bf16x3(const ContractArgs &a, const uint16_t *bank_h
                                    cudaStream_t stream, int64_t *launches) {
   if (!bf16x3_launchable(a)) return cudaErrorNotSupported;
   // launches whose CTAs walk more than two tiles run on CTA pairs (k4p_block_lmmse_pair.cu: cta_group::2, M = 256)
-  if (bf16x3_pair_wanted(a)) return launch_contract_bf16x3_pair(a, bank_hi, bank_lo, stream, launches);
+  if (bf16x3_pair_wanted(a)) {
+    const cudaError_t ep = launch_contract_bf16x3_pair(a, bank_hi, bank_lo, stream, launches);
+    if (ep == cudaSuccess) return ep;
+    (void)cudaGetLastError();   // a refused cluster launch is not sticky: fall through to single CTAs
+  }
   if (a.n_win <= MAXW_PARAM && a.geo_host == nullptr) return cudaErrorInvalidValue;
   DevInfo *di = nullptr;
   cudaError_t e = dev_info(&di);

@@ -166,7 +166,7 @@ struct Tile4 {
 __device__ __forceinline__ Tile4 decode4(const K4Params &p, int g, int rank = 0) {
   Tile4 ti;
   // column block fastest (measured faster than window-fastest on configs 3-5)
-  ti.ct = p.pair ? 2 * (g % p.n_ct) + rank : g % p.n_ct;
+  ti.ct = 2 * (g % p.n_ct) + rank;   // CTA rank r of a pair takes the 128-row tile 2 * (pair tile) + r
   const int rest = g / p.n_ct;
   const int w = rest % p.n_win;
   ti.t = rest / p.n_win;
