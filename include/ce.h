@@ -61,7 +61,9 @@ typedef enum {
   CE_KERNEL_SIMT = 1,   /* K2: FP32 SIMT complex FMA contraction (fallback when the tensor-core filter banks do not
                            fit; north_star's SIMT design, kept for parity and as the FP32 reference path) */
   CE_KERNEL_TF32X3 = 2, /* K3: tcgen05 kind::tf32, error-compensated hi/lo split (3 MMAs) */
-  CE_KERNEL_BF16X3 = 3  /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring */
+  CE_KERNEL_BF16X3 = 3  /* K4: tcgen05 kind::f16 (BF16), hi/lo split (3 MMAs), TMA-fed input ring; launches whose CTAs
+                           walk more than two tiles run its CTA-pair variant (cta_group::2, M = 256, half of each
+                           filter chunk per CTA): the same products in the same order, still reported as BF16X3 */
   /* 4 was the CTA-pair kernel K5 (filter stationary in TMEM): removed in round 2 -- exact, but pair MMAs with the
    * A operand in TMEM cost 180 cycles flat and it ran 2.6-4.5x slower than K4; 4 is now CE_EINVAL */
 } ce_kernel;
