@@ -11,6 +11,7 @@ v8_gfirst_param  v2 with the stride from the kernel parameters
 v9_sraw       p.s_raw re-read at each use
 v10_nks       the MMA K-step count computed inside the MMA role instead of at the kernel top
 v12_srstep    the transform's raw-ring slot and phase stepped instead of divided out of the chunk counter
+v13_prodstep  the same in the raw producer (two integer divisions less before the first TMA issue)
 """
 import os
 
@@ -86,6 +87,13 @@ def main():
     v["v12_srstep"] = must(s, "        if (tid == 0 && it < 24) K4TR(56 + it);\n        mbar_arrive(&a_full[sa]);\n      }",
                            "        if (tid == 0 && it < 24) K4TR(56 + it);\n        mbar_arrive(&a_full[sa]);\n"
                            "        if (++sr == S_RAW) {\n          sr = 0;\n          phr ^= 1u;\n        }\n      }")
+    s = must(base, "      const uint32_t xbytes = uint32_t(xbytes0);\n      int it = 0;\n",
+             "      const uint32_t xbytes = uint32_t(xbytes0);\n      int it = 0, s = 0;\n      uint32_t phe = 1;\n")
+    s = must(s, "          const int s = it % S_RAW;\n          mbar_wait(&raw_empty[s], ((it / S_RAW) & 1) ^ 1);\n#ifdef CE_K4_TRACE\n          if (it == 0) c_w0",
+             "          mbar_wait(&raw_empty[s], phe);\n#ifdef CE_K4_TRACE\n          if (it == 0) c_w0")
+    v["v13_prodstep"] = must(s, "            tma_load_2d(raw + s * RAW_STAGE + RAWY, &tmx, f0, ti.t * K0, &raw_full[s]);\n        }",
+                             "            tma_load_2d(raw + s * RAW_STAGE + RAWY, &tmx, f0, ti.t * K0, &raw_full[s]);\n"
+                             "          if (++s == S_RAW) {\n            s = 0;\n            phe ^= 1u;\n          }\n        }")
     for name, text in v.items():
         with open(os.path.join(OUT, name + ".cu"), "w") as f:
             f.write(text)
