@@ -458,6 +458,21 @@ def _device_inputs(cfg, m_lo, m_hi, dev, seed=11):
     return make_y
 
 
+def _k4_variant(sel, cfg, m_local, props):
+    """The K4 launch shape the library's policy picks for this call (mirrors bf16x3_pair_wanted in
+    csrc/k4p_block_lmmse_pair.cu, CE_K4_PAIR overrides it): CTA pairs (tcgen05 cta_group::2) when every CTA walks
+    more than two 128-row tiles, single CTAs otherwise.  Windows too wide for one accumulator (config 6) are split
+    by the library; the unsplit count used here only matters at that boundary."""
+    if sel != 3:
+        return None
+    import paper_1802_05427_b200 as ce
+    n_ct = -(-m_local * cfg.K // 128)
+    n_win = len(ce.ce_window_table(cfg.N, cfg.b, cfg.stride))
+    env = os.environ.get("CE_K4_PAIR")
+    pair = n_ct >= 2 and (env == "1" if env in ("0", "1") else cfg.T * n_win * n_ct > 2 * props.multi_processor_count)
+    return "k4_bf16x3_pair (clusters of two CTAs, cta_group::2)" if pair else "k4_bf16x3 (single CTAs)"
+
+
 def sweep_line(cfg_id, args, dist, peaks, props, sm_max):
     """Device-time line of another configuration (strong-scaled: its own M antennas split across the ranks)."""
     import torch
@@ -483,7 +498,8 @@ def sweep_line(cfg_id, args, dist, peaks, props, sm_max):
             "steps": args.sweep_steps, "warmup": 3, "ms_per_step": res["ms_max"] / args.sweep_steps,
             "per_rank_ms_per_step": [v / args.sweep_steps for v in res["ms_ranks"]],
             "value": cfg.estimates * args.sweep_steps / (res["ms_max"] * 1e-3), "unit": "estimates/s",
-            "kernel": KERNEL_NAMES.get(sel), "dtype": KERNEL_DTYPE.get(sel),
+            "kernel": KERNEL_NAMES.get(sel), "kernel_variant": _k4_variant(sel, cfg, m_hi - m_lo, props),
+            "dtype": KERNEL_DTYPE.get(sel),
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "roofline_time_us")},
             "gpu_launches": res["launches"], "clocks": res["clocks"],
             "l2": f"rotating {nbuf} y/h buffer pairs (> L2)", "data": "y drawn on device (timing only), seeded pilots"}
@@ -669,6 +685,7 @@ def run_ours(args, cfg):
             "config": _cfg_json(cfg, {"l2": f"inputs larger than L2: rotating {nbuf} y/h buffer pairs "
                                             f"({nbuf * 2 * y.nbytes / 2**20:.0f} MiB > 126 MiB)",
                                       "kernel": KERNEL_NAMES[args.kernel] + f"->{KERNEL_NAMES.get(sel)}",
+                                      "kernel_variant": _k4_variant(sel, cfg, M, props),
                                       "launch": args.launch, "global_antennas": M_glob,
                                       "parallelism": f"antenna shard x{world} ({dist.backend}), no data-path collective"}),
             "roofline": roof,
