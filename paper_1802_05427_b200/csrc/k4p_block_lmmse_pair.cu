@@ -792,7 +792,9 @@ extern "C" int ce_k4p_trace_set(void *dptr) {
 // Policy.  CE_K4_PAIR = 0 / 1 forces pairs off / on (experiments).  Default: pairs when every CTA walks more than two
 // 128-row tiles.  Measured, same box, against K4 (two repetitions each): config 5 1486-1488 -> 1400-1435 us
 // (-3.5..6 %), config 4 325-330 -> 314-323 us (-1..5 %); config 3 (one tile per SM) 9.9 -> 11.6 us (the cluster
-// barrier in the prologue, chunk lockstep of the two CTAs).  The power mode keeps single CTAs (not measured in pairs).
+// barrier in the prologue, chunk lockstep of the two CTAs).  The power mode (the statistics noise window: N = 64, no
+// stores) keeps single CTAs: exact in pairs, but the statistics step measured 571 -> 587 us (config 4), 2120 -> 2200 us
+// (config 5).
 bool bf16x3_pair_wanted(const ContractArgs &a) {
   static const int env_pair = getenv("CE_K4_PAIR") ? atoi(getenv("CE_K4_PAIR")) : -1;
   if (env_pair == 0) return false;
