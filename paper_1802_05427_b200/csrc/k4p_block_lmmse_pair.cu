@@ -35,7 +35,7 @@
 // on two adjacent 128-row tiles of the same (instance, window) as ONE tcgen05 cta_group::2 MMA of M = 256.  Each
 // CTA transforms its own rows into its own A stage and fetches HALF of the filter chunk's rows (the pair's MMA
 // reads both halves in place), so the filter-bank stream per SM and the B bytes each MMA reads from shared memory
-// halve; A and B keep rings of their own (3 A stages of 16 KB, 5 B stages of 16 KB, 4 raw stages).  The leader (rank 0)
+// halve; A and B keep rings of their own (4 A stages of 16 KB, 4 B stages of 16 KB, 4 raw stages).  The leader (rank 0)
 // issues every MMA; its a_full / tmem_empty barriers count the warps of both CTAs (one arrive per warp, the peer's
 // through mapa + mbarrier.arrive on the leader's barrier), the peer's MMA warp forwards "my half of the chunk has
 // landed" (bulk copies can only signal a barrier of their own CTA), and the commits are multicast to both CTAs.
@@ -114,10 +114,10 @@ constexpr int B_PLANE_P = B_PLANE / 2;     // 8 KB
 constexpr int A_STAGE_P = 2 * A_PLANE;     // 16 KB: A_hi | A_lo
 constexpr int B_STAGE_P = 2 * B_PLANE_P;   // 16 KB: this CTA's half of B_hi | B_lo
 #ifndef K4_S_AB_P
-#define K4_S_AB_P 3          // A stages in pair mode
+#define K4_S_AB_P 4          // A stages in pair mode (4 + 4: config 5 1395-1399 us; 3 + 5: 1406-1427; 2 + 6: 1402)
 #endif
 #ifndef K4_S_B_P
-#define K4_S_B_P 5           // filter-chunk stages in pair mode
+#define K4_S_B_P 4           // filter-chunk stages in pair mode
 #endif
 #ifndef K4_EPI_DB_P
 #define K4_EPI_DB_P 0        // experiments: 1 = two staging boxes per epilogue warp in pair mode
